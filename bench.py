@@ -1,0 +1,463 @@
+#!/usr/bin/env python
+"""Bench harness: SK-net labeling throughput (labels/s) on B200, the metric of the paper's
+headline table (`throughput px_per_s`, proj/tools/pixelseg.cpp:259-262).
+
+One step = process() of one 1024x1024 synthetic u8 image per GPU through full sk.net with the
+reference's tiling (w = 128 output tiles, v = 101 context; pipeline.hpp:630-698), fp64-exact:
+labels and probability planes bit-identical to the reference's. Weak scaling: every rank owns
+one image; for N > 1 the per-image results are gathered to rank 0 over NCCL (the only
+collective -- the final combine).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+`value` is device-resident throughput (image already in HBM); `e2e` is the same through the C
+ABI with pinned host buffers (H2D of the image, D2H of labels + probs inside the timed region).
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, the unmodified
+reference headers; else the C restatement) on all host cores, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PUBLISHED_SK_LABELS_PER_S = 85460.0  # GTX 980 CUDA+cuBLAS
+V = 101  # sk.net context surplus (229 - 128)
+
+
+def sk_text() -> str:
+    f = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
+    return bytes(f["sk"]).decode()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ CPU baseline
+def cpu_reference_sample(threads: int, w_out: int, seed_img: int = 55):
+    """The reference's own NetRunner<float>::forward (oracle/_ref) -- or the C restatement when
+    _ref is absent -- on `threads` host threads at once, each over one w_out x w_out tile of
+    process()'s tiling of the workload image. Returns (labels, wall_s, flops, kind)."""
+    from oracle import oracle as O
+
+    import paper_1509_03371_b200 as g
+
+    text = sk_text()
+    spec = g.parse_netspec_or_throw(text)
+    w0 = w_out + V
+    img = g.Rng(seed_img).index_array_u8(1024 * 1024, 256).reshape(1024, 1024)
+    padded = O.normalize(O.mirror_pad(img, V))
+    kind = "reference" if O.ref_available() else "port"
+    nets = []
+    for t in range(threads):
+        oy, ox = (t * w_out) % (1024 - w_out), ((t * 7 + 3) * w_out) % (1024 - w_out)
+        x = np.ascontiguousarray(np.broadcast_to(padded[oy:oy + w0, ox:ox + w0], (3, w0, w0)))
+        if kind == "reference":
+            nets.append((O.RefNet(text, seed=1), x))
+        else:
+            nets.append((O.init_weights(spec, 1), x))
+    errs = []
+
+    def work(i):
+        try:
+            net, x = nets[i]
+            if kind == "reference":
+                net.forward(x)
+            else:
+                O.forward_net(spec, net, x)
+        except Exception as e:  # pragma: no cover
+            errs.append(e)
+
+    ths = [threading.Thread(target=work, args=(i,)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    wall = time.perf_counter() - t0
+    if errs:
+        raise errs[0]
+    flops = g.flop_estimate(spec, w0)["total"] * threads
+    return threads * w_out * w_out, wall, flops, kind
+
+
+def cpu_baseline_obj(threads: int, w_out: int):
+    import paper_1509_03371_b200 as g
+
+    labels, wall, flops, kind = cpu_reference_sample(threads, w_out)
+    spec = g.parse_netspec_or_throw(sk_text())
+    flop_per_label_workload = g.flop_estimate(spec, 128 + V)["total"] / (128 * 128)
+    measured = labels / wall
+    scaled = (flops / wall) / flop_per_label_workload
+    return {
+        "value": scaled,
+        "unit": "labels/s",
+        "cores": threads,
+        "kind": kind,
+        "sample": (f"{threads} threads x one sk.net forward of a {w_out}x{w_out}-label tile "
+                   f"(input {w_out + V}) of the workload image, concurrently; measured "
+                   f"{measured:.3f} labels/s = {flops / wall / 1e9:.2f} GFLOP/s, scaled to the "
+                   f"workload's 128-tile FLOP/label ({flop_per_label_workload / 1e6:.2f} MFLOP)"),
+        "sample_labels_per_s": measured,
+        "sample_seconds": wall,
+    }
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    threads = args.cpu_threads or os.cpu_count() or 1
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline_obj(threads, args.cpu_tile)
+        if i >= args.warmup:
+            vals.append(cb)
+    value = statistics.mean(v["value"] for v in vals)
+    ms_per_step = statistics.mean(v["sample_seconds"] for v in vals) * 1e3
+    cb = dict(vals[-1])
+    cb["value"] = value
+    line = {
+        "impl": "reference",
+        "metric": "labels/s",
+        "value": value,
+        "unit": "labels/s",
+        "n_gpus": args.gpus,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": value / PUBLISHED_SK_LABELS_PER_S,
+        "dtype": "f64",
+        "data": "synthetic: Rng(55) u8 image, init_weights(sk.net, seed 1)",
+        "config": workload_config(args, 1),
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "labels/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args, n):
+    return {
+        "workload": (f"sk.net process(): {args.size}x{args.size} synthetic u8 image per GPU, "
+                     f"tile w={args.tile}, v={V} (pipeline.hpp:630-698), fp64-exact"),
+        "net": "sk.net (proj/configs)",
+        "image": [args.size, args.size],
+        "tile": args.tile,
+        "images_per_step": n,
+        "labels_per_step": n * args.size * args.size,
+        "l2": "flushed between steps (256 MiB device write)",
+        "parallelism": f"dp{n} (one image per GPU; NCCL gather of labels+probs to rank 0)",
+    }
+
+
+# ------------------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+
+    import paper_1509_03371_b200 as g
+    from paper_1509_03371_b200 import _lib
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    _lib.check(_lib.lib().graft_set_device(local))
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    spec = g.parse_netspec_or_throw(sk_text())
+    states = g.init_weights(spec, 1)
+    proc = g.Processor(spec, states, tile_batch=args.tile_batch)
+    net = proc.net.h
+    C = proc.n_classes
+    H = W = args.size
+    w = args.tile
+    img = g.Rng(55 + rank).index_array_u8(H * W, 256).reshape(H, W)
+    dev = torch.device("cuda", local)
+    img_d = torch.from_numpy(img).to(dev)
+    lab_d = torch.empty((H, W), dtype=torch.uint8, device=dev)
+    prob_d = torch.empty((C, H, W), dtype=torch.float32, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.ExternalStream(_lib.lib().graft_net_stream(net), device=dev)
+    if ws > 1:
+        gl = [torch.empty_like(lab_d) for _ in range(ws)] if rank == 0 else None
+        gp = [torch.empty_like(prob_d) for _ in range(ws)] if rank == 0 else None
+
+    def combine():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.gather(lab_d, gl, dst=0)
+            dist.gather(prob_d, gp, dst=0)
+
+    def step_device():
+        proc.run(img_d, w, V, lab_d, prob_d, mem=_lib.MEM_DEVICE)
+        combine()
+
+    # measured FP64 (DMMA) peak, sustained, for the roofline denominator
+    import ctypes
+
+    pk = ctypes.c_double()
+    _lib.check(_lib.lib().graft_fp64_peak(2.0, ctypes.byref(pk)))
+    peak_sustained = pk.value
+
+    for _ in range(args.warmup):
+        step_device()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---- timed: device-resident ----
+    proc.net.set_option(_lib.OPT_TIMED, 1)
+    _lib.check(_lib.lib().graft_net_reset_stats(net))
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.lib().graft_launch_count()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step_device()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    launches = _lib.lib().graft_launch_count() - launches0
+    clk = clocks.stop()
+    proc.net.set_option(_lib.OPT_TIMED, 0)
+    L = len(spec.layers)
+    ms = (ctypes.c_double * L)()
+    runs = (ctypes.c_longlong * L)()
+    _lib.check(_lib.lib().graft_net_layer_stats(net, ms, runs, L))
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    labels_total = ws * H * W * args.steps
+    value = labels_total / (total_ms * 1e-3)
+
+    # ---- timed: e2e through the C ABI with pinned host buffers ----
+    img_h = torch.from_numpy(img).pin_memory()
+    lab_h = torch.empty((H, W), dtype=torch.uint8).pin_memory()
+    prob_h = torch.empty((C, H, W), dtype=torch.float32).pin_memory()
+    if ws > 1:
+        gl_h = torch.empty((ws, H, W), dtype=torch.uint8).pin_memory() if rank == 0 else None
+        gp_h = torch.empty((ws, C, H, W), dtype=torch.float32).pin_memory() if rank == 0 else None
+
+    def step_e2e():
+        if ws == 1:
+            _lib.check(_lib.lib().graft_process(net, img_h.data_ptr(), H, W, w, V,
+                                                lab_h.data_ptr(), prob_h.data_ptr(),
+                                                _lib.MEM_HOST))
+        else:
+            img_d.copy_(img_h, non_blocking=True)
+            torch.cuda.current_stream().synchronize()
+            proc.run(img_d, w, V, lab_d, prob_d, mem=_lib.MEM_DEVICE)
+            combine()
+            if rank == 0:
+                for r in range(ws):
+                    gl_h[r].copy_(gl[r], non_blocking=True)
+                    gp_h[r].copy_(gp[r], non_blocking=True)
+                torch.cuda.current_stream().synchronize()
+
+    step_e2e()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        t0 = time.perf_counter()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        step_e2e()
+        e1.record(stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        e2e_ms += max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_value = labels_total / (float(t.item()) * 1e-3)
+    # parity spot check of the e2e result against the device result (same image)
+    proc.run(img_d, w, V, lab_d, prob_d, mem=_lib.MEM_DEVICE)
+    if ws == 1:
+        assert np.array_equal(lab_h.numpy(), lab_d.cpu().numpy())
+
+    if rank != 0:
+        if ws > 1:
+            import torch.distributed as dist
+
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (ip1's conv_exact launches) ----
+    names = [l.name for l in spec.layers]
+    ip1 = names.index("ip1")
+    fl = g.flop_estimate(spec, w + V)
+    n_tiles = g.tile_rows(H, w) * g.tile_rows(W, w)
+    ip1_flops_total = fl["ip1"] * n_tiles * args.steps
+    ip1_ms = ms[ip1]
+    achieved = ip1_flops_total / (ip1_ms * 1e-3) / 1e12 if ip1_ms > 0 else None
+    conv_ms = sum(ms[i] for i, l in enumerate(spec.layers) if l.kind == g.LayerKind.ConvSK)
+    all_ms = sum(ms[i] for i in range(L))
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "conv_ip1_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            tj = json.load(f)
+        traffic = tj.get("bytes_per_launch")
+    roofline = {
+        "bound": "tensor",
+        "pipe": "fp64 tensor (DMMA.8x8x4)",
+        "achieved": achieved,
+        "peak": peak_sustained,
+        "peak_source": "measured live in bench.py: graft_fp64_peak (DMMA issue loop, 2 s sustained); "
+                       "MEASURED_PEAKS.json has no FP64 figure",
+        "unit": "TFLOP/s",
+        "frac": achieved / peak_sustained if achieved else None,
+        "traffic": traffic,
+        "kernel": "conv_exact_kernel (ip1: M=1024, K=19200, 16384 px/tile)",
+        "flops_per_launch": fl["ip1"] * n_tiles * args.steps / max(1, runs[ip1]),
+        "avg_launch_ms": ip1_ms / max(1, runs[ip1]),
+        "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
+        "conv_share_of_step": conv_ms / all_ms if all_ms else None,
+        "whole_net_tflops": fl["total"] * n_tiles * args.steps / (total_ms * 1e-3) / 1e12,
+    }
+    line = {
+        "metric": "labels/s",
+        "value": value,
+        "unit": "labels/s",
+        "n_gpus": ws,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": value / PUBLISHED_SK_LABELS_PER_S,
+        "dtype": "f64",
+        "data": "synthetic: Rng(55+rank) u8 image per GPU; weights init_weights(sk.net, seed 1)",
+        "config": workload_config(args, ws),
+        "e2e": {"value": e2e_value, "unit": "labels/s", "h2d_bytes_per_step": ws * H * W,
+                "d2h_bytes_per_step": ws * H * W * (1 + 4 * C)},
+        "gpu_launches": int(launches),
+        "clocks": clk,
+        "roofline": roofline,
+        "layer_ms_per_step": {names[i]: ms[i] / args.steps for i in range(1, L) if ms[i] > 0},
+    }
+    if ws == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline_obj(args.cpu_threads or os.cpu_count() or 1,
+                                                args.cpu_tile)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--size", type=int, default=1024)
+    ap.add_argument("--tile", type=int, default=128)
+    ap.add_argument("--tile-batch", type=int, default=0)
+    ap.add_argument("--cpu-tile", type=int, default=4, help="labels per side of a CPU sample tile")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,428 @@
+"""Python face of the CPU checker -- TEST INFRASTRUCTURE ONLY.
+
+Two independent CPU routes, both loaded with ctypes:
+  * ``C``   -- liboracle.so, the plain-C restatement (oracle/pixelseg_oracle.c), and a small
+               Python net executor over it (``forward_net``, ``process``) that restates
+               NetRunner::forward (netgraph.hpp:64-84, 129-165) and process
+               (pipeline.hpp:630-698);
+  * ``REF`` -- oracle/_ref/libpixelseg_ref.so, the unmodified reference headers compiled from
+               /root/reference by oracle/Makefile (absent on the GPU box unless shipped).
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs may
+import this module, and only as the checker or the timed CPU baseline -- never as product.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libpixelseg_ref.so")
+
+_vp, _i, _u64, _d, _f, _sz = C.c_void_p, C.c_int, C.c_uint64, C.c_double, C.c_float, C.c_size_t
+
+_ORC_SIGS = {
+    "orc_last_error": (C.c_char_p, []),
+    "orc_rng_state_size": (_sz, []),
+    "orc_rng_seed": (None, [_vp, _u64]),
+    "orc_rng_next_u64": (_u64, [_vp]),
+    "orc_rng_uniform01": (_d, [_vp]),
+    "orc_rng_uniform": (_d, [_vp, _d, _d]),
+    "orc_rng_gaussian": (_d, [_vp]),
+    "orc_rng_fill_uniform_f32": (None, [_vp, _vp, _sz, _d, _d]),
+    "orc_rng_fill_uniform_f64": (None, [_vp, _vp, _sz, _d, _d]),
+    "orc_rng_fill_gaussian_f32": (None, [_vp, _vp, _sz, _d, _d]),
+    "orc_rng_fill_gaussian_f64": (None, [_vp, _vp, _sz, _d, _d]),
+    "orc_rng_fill_index_u8": (None, [_vp, _vp, _sz, _u64]),
+    "orc_out_extent": (_i, [_i, _i, _i, _i, _i, C.c_char_p, C.POINTER(_i)]),
+    "orc_im2col_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "orc_im2col_f64": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "orc_gemm_f32": (None, [_i, _i, _i, _i, _i, _f, _vp, _vp, _f, _vp]),
+    "orc_gemm_f64": (None, [_i, _i, _i, _i, _i, _d, _vp, _vp, _d, _vp]),
+    "orc_conv_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "orc_conv_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "orc_conv_f32_mt": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp, _i]),
+    "orc_maxpool_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "orc_maxpool_f64": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "orc_relu_f32": (None, [_vp, _sz, _vp]),
+    "orc_relu_f64": (None, [_vp, _sz, _vp]),
+    "orc_upconv_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "orc_upconv_f64": (None, [_vp, _i, _i, _i, _vp]),
+    "orc_mergecrop_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _i, _vp]),
+    "orc_mergecrop_f64": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _i, _vp]),
+    "orc_softmax_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "orc_softmax_f64": (None, [_vp, _i, _i, _i, _vp]),
+    "orc_mirror_pad_u8": (_i, [_vp, _i, _i, _i, _vp]),
+    "orc_normalize_f32": (None, [_vp, _sz, _vp]),
+    "orc_tile_offsets": (_i, [_i, _i, C.POINTER(_i), _i]),
+    "orc_stitch_f32": (None, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+}
+
+_REF_SIGS = {
+    "ref_last_error": (C.c_char_p, []),
+    "ref_im2col_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "ref_gemm_f32": (None, [_i, _i, _i, _i, _i, _f, _vp, _vp, _f, _vp]),
+    "ref_gemm_f64": (None, [_i, _i, _i, _i, _i, _d, _vp, _vp, _d, _vp]),
+    "ref_conv_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "ref_conv_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, _i, _i, _i, _i, _i, _vp]),
+    "ref_maxpool_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "ref_relu_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "ref_upconv_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "ref_mergecrop_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _i, _vp]),
+    "ref_softmax_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "ref_mirror_pad_u8": (_i, [_vp, _i, _i, _i, _vp]),
+    "ref_normalize_f32": (None, [_vp, _i, _vp]),
+    "ref_net_create": (_vp, [C.c_char_p]),
+    "ref_net_destroy": (None, [_vp]),
+    "ref_correct_sw": (_i, [C.c_char_p, C.c_char_p, _i]),
+    "ref_net_init_weights": (_i, [_vp, _u64]),
+    "ref_net_num_layers": (_i, [_vp]),
+    "ref_net_param_sizes": (None, [_vp, _i, C.POINTER(C.c_longlong), C.POINTER(C.c_longlong)]),
+    "ref_net_get_params": (None, [_vp, _i, _vp, _vp]),
+    "ref_net_set_params": (None, [_vp, _i, _vp, _vp]),
+    "ref_net_set_layer_fout": (_i, [_vp, C.c_char_p, _i, _d]),
+    "ref_net_output_extent": (_i, [_vp, _i, C.POINTER(_i)]),
+    "ref_net_flops": (C.c_longlong, [_vp, _i]),
+    "ref_net_forward": (_i, [_vp, _vp, _i, _i, _i, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "ref_net_blob_shape": (_i, [_vp, C.c_char_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
+    "ref_net_blob": (_i, [_vp, C.c_char_p, _vp]),
+    "ref_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+}
+
+
+def _load(path, sigs):
+    lib = C.CDLL(path)
+    for name, (res, args) in sigs.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+_orc = None
+_ref = None
+
+
+def orc():
+    global _orc
+    if _orc is None:
+        if not os.path.exists(ORACLE_SO):
+            raise ImportError(f"{ORACLE_SO} missing: run `make -C oracle`")
+        _orc = _load(ORACLE_SO, _ORC_SIGS)
+    return _orc
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref():
+    global _ref
+    if _ref is None:
+        _ref = _load(REF_SO, _REF_SIGS)
+    return _ref
+
+
+def p(a):
+    return None if a is None else a.ctypes.data
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def _chk(rc, lib_err):
+    if rc:
+        raise OracleError(rc, lib_err().decode())
+
+
+# ---------------- Rng (rng.hpp) ----------------
+class Rng:
+    def __init__(self, seed: int):
+        self.buf = C.create_string_buffer(orc().orc_rng_state_size())
+        orc().orc_rng_seed(self.buf, C.c_uint64(seed & (2**64 - 1)))
+
+    def uniform(self, lo=None, hi=None):
+        if lo is None:
+            return orc().orc_rng_uniform01(self.buf)
+        return orc().orc_rng_uniform(self.buf, lo, hi)
+
+    def next_u64(self):
+        return orc().orc_rng_next_u64(self.buf)
+
+    def gaussian(self):
+        return orc().orc_rng_gaussian(self.buf)
+
+    def uniform_f32(self, n, lo=-1.0, hi=1.0):
+        a = np.empty(n, np.float32)
+        orc().orc_rng_fill_uniform_f32(self.buf, p(a), n, lo, hi)
+        return a
+
+    def uniform_f64(self, n, lo=-1.0, hi=1.0):
+        a = np.empty(n, np.float64)
+        orc().orc_rng_fill_uniform_f64(self.buf, p(a), n, lo, hi)
+        return a
+
+    def gaussian_f32(self, n, mean, sigma):
+        a = np.empty(n, np.float32)
+        orc().orc_rng_fill_gaussian_f32(self.buf, p(a), n, mean, sigma)
+        return a
+
+    def index_u8(self, n, m=256):
+        a = np.empty(n, np.uint8)
+        orc().orc_rng_fill_index_u8(self.buf, p(a), n, m)
+        return a
+
+
+# ---------------- layers (C restatement) ----------------
+def _sfx(a):
+    return "f64" if a.dtype == np.float64 else "f32"
+
+
+def out_extent(in_, k, d, s, p_, what="extent"):
+    o = C.c_int()
+    _chk(orc().orc_out_extent(in_, k, d, s, p_, what.encode(), C.byref(o)), orc().orc_last_error)
+    return o.value
+
+
+def conv(x, w, b, f_out, k, d=1, s=1, p_=0, threads=1):
+    """x: (C,H,W); w: (f_out*C*k*k,); b: (f_out,) -> (f_out, oh, ow)."""
+    x = np.ascontiguousarray(x)
+    Cc, H, W = x.shape
+    oh, ow = out_extent(H, k, d, s, p_, "height"), out_extent(W, k, d, s, p_, "width")
+    out = np.empty((f_out, oh, ow), x.dtype)
+    w = np.ascontiguousarray(w, x.dtype)
+    b = np.ascontiguousarray(b, x.dtype)
+    if x.dtype == np.float32 and threads > 1:
+        rc = orc().orc_conv_f32_mt(p(x), Cc, H, W, p(w), p(b), f_out, k, d, s, p_, p(out), threads)
+    else:
+        rc = getattr(orc(), "orc_conv_" + _sfx(x))(p(x), Cc, H, W, p(w), p(b), f_out, k, d, s, p_,
+                                                    p(out))
+    _chk(rc, orc().orc_last_error)
+    return out
+
+
+def im2col(x, k, d=1, s=1, p_=0):
+    x = np.ascontiguousarray(x)
+    Cc, H, W = x.shape
+    oh, ow = out_extent(H, k, d, s, p_, "height"), out_extent(W, k, d, s, p_, "width")
+    col = np.empty((Cc * k * k, oh * ow), x.dtype)
+    _chk(getattr(orc(), "orc_im2col_" + _sfx(x))(p(x), Cc, H, W, k, d, s, p_, p(col)),
+         orc().orc_last_error)
+    return col
+
+
+def gemm(ta, tb, m, n, k, alpha, a, b, beta, c):
+    getattr(orc(), "orc_gemm_" + _sfx(c))(int(ta), int(tb), m, n, k, alpha, p(a), p(b), beta, p(c))
+
+
+def maxpool(x, k, d=1, s=1, want_argmax=False):
+    x = np.ascontiguousarray(x)
+    Cc, H, W = x.shape
+    oh, ow = out_extent(H, k, d, s, 0, "height"), out_extent(W, k, d, s, 0, "width")
+    out = np.empty((Cc, oh, ow), x.dtype)
+    am = np.empty(out.size, np.uint64) if want_argmax else None
+    _chk(getattr(orc(), "orc_maxpool_" + _sfx(x))(p(x), Cc, H, W, k, d, s, p(out), p(am)),
+         orc().orc_last_error)
+    return (out, am) if want_argmax else out
+
+
+def relu(x):
+    x = np.ascontiguousarray(x)
+    out = np.empty_like(x)
+    getattr(orc(), "orc_relu_" + _sfx(x))(p(x), x.size, p(out))
+    return out
+
+
+def upconv(x):
+    x = np.ascontiguousarray(x)
+    Cc, H, W = x.shape
+    out = np.empty((Cc, 2 * H, 2 * W), x.dtype)
+    getattr(orc(), "orc_upconv_" + _sfx(x))(p(x), Cc, H, W, p(out))
+    return out
+
+
+def mergecrop(a, b):
+    a, b = np.ascontiguousarray(a), np.ascontiguousarray(b)
+    out = np.empty((a.shape[0] + b.shape[0], a.shape[1], a.shape[2]), a.dtype)
+    _chk(getattr(orc(), "orc_mergecrop_" + _sfx(a))(p(a), *a.shape, p(b), *b.shape, p(out)),
+         orc().orc_last_error)
+    return out
+
+
+def softmax(x):
+    x = np.ascontiguousarray(x)
+    out = np.empty_like(x)
+    getattr(orc(), "orc_softmax_" + _sfx(x))(p(x), *x.shape, p(out))
+    return out
+
+
+def mirror_pad(img, v):
+    img = np.ascontiguousarray(img, np.uint8)
+    H, W = img.shape
+    out = np.empty((H + v, W + v), np.uint8)
+    _chk(orc().orc_mirror_pad_u8(p(img), H, W, v, p(out)), orc().orc_last_error)
+    return out
+
+
+def normalize(img):
+    img = np.ascontiguousarray(img, np.uint8)
+    out = np.empty(img.shape, np.float32)
+    orc().orc_normalize_f32(p(img), img.size, p(out))
+    return out
+
+
+def tile_offsets(extent, w):
+    buf = (C.c_int * 4096)()
+    n = orc().orc_tile_offsets(extent, w, buf, 4096)
+    return [buf[i] for i in range(n)]
+
+
+# ---------------- net executor over the C restatement ----------------
+def init_weights(spec, seed):
+    """init_weights<float> (netgraph.hpp:27-46) over the oracle Rng; spec is a
+    paper_1509_03371_b200.netspec.NetSpec (host config only)."""
+    from paper_1509_03371_b200.netspec import InitKind, compute_channels
+
+    rng = Rng(seed)
+    ch = compute_channels(spec)
+    params: Dict[int, tuple] = {}
+    for i, l in enumerate(spec.layers):
+        if not l.has_weights():
+            continue
+        fan_in = sum(ch[b] for b in l.inputs) * l.k * l.k
+        sigma = l.init_sigma
+        if l.init == InitKind.He:
+            sigma = float(np.sqrt(2.0 / float(fan_in)))
+        if l.init == InitKind.None_:
+            sigma = 0.01
+        w = rng.gaussian_f32(l.f_out * fan_in, 0.0, sigma)
+        params[i] = (w, np.zeros(l.f_out, np.float32))
+    return params
+
+
+def forward_net(spec, params, x, threads=1, keep=False):
+    """NetRunner<float>::forward restated over the C layers. Returns the last blob, or the
+    whole blob table when keep=True."""
+    from paper_1509_03371_b200.netspec import LayerKind
+
+    blobs: Dict[str, np.ndarray] = {}
+    for i, l in enumerate(spec.layers):
+        if l.kind == LayerKind.Data:
+            blobs[l.output] = np.ascontiguousarray(x, np.float32)
+        elif l.kind == LayerKind.ConvSK:
+            w, b = params[i]
+            blobs[l.output] = conv(blobs[l.inputs[0]], w, b, l.f_out, l.k, l.d, l.s, l.p,
+                                   threads=threads)
+        elif l.kind == LayerKind.PoolMax:
+            blobs[l.output] = maxpool(blobs[l.inputs[0]], l.k, l.d, l.s)
+        elif l.kind == LayerKind.Relu:
+            blobs[l.output] = relu(blobs[l.inputs[0]])
+        elif l.kind == LayerKind.Upconv:
+            blobs[l.output] = upconv(blobs[l.inputs[0]])
+        elif l.kind == LayerKind.MergeCrop:
+            blobs[l.output] = mergecrop(blobs[l.inputs[0]], blobs[l.inputs[1]])
+        elif l.kind == LayerKind.SoftmaxLoss:
+            blobs[l.output] = softmax(blobs[l.inputs[0]])
+    return blobs if keep else blobs[spec.layers[-1].output]
+
+
+def process(spec, params, img, w, v, threads=1):
+    """process<float> (pipeline.hpp:630-698) restated: labels (H,W) u8, probs (C,H,W) f32."""
+    img = np.ascontiguousarray(img, np.uint8)
+    H, W = img.shape
+    padded = normalize(mirror_pad(img, v))
+    labels = np.zeros((H, W), np.uint8)
+    probs = None
+    for oy in tile_offsets(H, w):
+        for ox in tile_offsets(W, w):
+            tile = padded[oy:oy + w + v, ox:ox + w + v]
+            x = np.ascontiguousarray(np.broadcast_to(tile, (spec.f0,) + tile.shape))
+            out = forward_net(spec, params, x, threads=threads)
+            if probs is None:
+                probs = np.zeros((out.shape[0], H, W), np.float32)
+            orc().orc_stitch_f32(p(np.ascontiguousarray(out)), out.shape[0], w, oy, ox, H, W,
+                                 p(labels), p(probs))
+    return labels, probs
+
+
+# ---------------- the reference itself (oracle/_ref) ----------------
+class RefNet:
+    """NetRunner<float> / process<float> of the unmodified reference (via ref_shim.cpp)."""
+
+    def __init__(self, text: str, seed: Optional[int] = None,
+                 fout: Optional[Dict[str, int]] = None, sigma: float = 0.0):
+        self.h = ref().ref_net_create(text.encode())
+        if not self.h:
+            raise OracleError(2, ref().ref_last_error().decode())
+        for name, f in (fout or {}).items():
+            _chk(ref().ref_net_set_layer_fout(self.h, name.encode(), f, sigma), ref().ref_last_error)
+        if seed is not None:
+            _chk(ref().ref_net_init_weights(self.h, seed), ref().ref_last_error)
+
+    def __del__(self):
+        try:
+            ref().ref_net_destroy(self.h)
+        except Exception:
+            pass
+
+    def params(self) -> Dict[int, tuple]:
+        out = {}
+        for i in range(ref().ref_net_num_layers(self.h)):
+            nw, nb = C.c_longlong(), C.c_longlong()
+            ref().ref_net_param_sizes(self.h, i, C.byref(nw), C.byref(nb))
+            if nw.value == 0 and nb.value == 0:
+                continue
+            w = np.empty(nw.value, np.float32)
+            b = np.empty(nb.value, np.float32)
+            ref().ref_net_get_params(self.h, i, p(w), p(b))
+            out[i] = (w, b)
+        return out
+
+    def set_params(self, params):
+        for i, (w, b) in params.items():
+            ref().ref_net_set_params(self.h, i, p(np.ascontiguousarray(w, np.float32)),
+                                     p(np.ascontiguousarray(b, np.float32)))
+
+    def forward(self, x):
+        x = np.ascontiguousarray(x, np.float32)
+        c, h, w = C.c_int(), C.c_int(), C.c_int()
+        _chk(ref().ref_net_forward(self.h, p(x), *x.shape, C.byref(c), C.byref(h), C.byref(w)),
+             ref().ref_last_error)
+        return self.blob_shape_last(c.value, h.value, w.value)
+
+    def blob_shape_last(self, c, h, w):
+        return (c, h, w)
+
+    def blob(self, name: str) -> np.ndarray:
+        c, h, w = C.c_int(), C.c_int(), C.c_int()
+        _chk(ref().ref_net_blob_shape(self.h, name.encode(), C.byref(c), C.byref(h), C.byref(w)),
+             ref().ref_last_error)
+        out = np.empty((c.value, h.value, w.value), np.float32)
+        _chk(ref().ref_net_blob(self.h, name.encode(), p(out)), ref().ref_last_error)
+        return out
+
+    def process(self, img, w, v):
+        img = np.ascontiguousarray(img, np.uint8)
+        H, W = img.shape
+        labels = np.zeros((H, W), np.uint8)
+        # class count = channels of the last blob; probe with a forward-free query is not
+        # exposed, so allocate for up to 256 classes and trim by the caller's knowledge.
+        probs = np.zeros((self.n_classes, H, W), np.float32)
+        _chk(ref().ref_process(self.h, p(img), H, W, w, v, p(labels), p(probs)),
+             ref().ref_last_error)
+        return labels, probs
+
+    n_classes = 2
+
+
+def correct_sw(text: str) -> str:
+    buf = C.create_string_buffer(1 << 16)
+    _chk(ref().ref_correct_sw(text.encode(), buf, len(buf)), ref().ref_last_error)
+    return buf.value.decode()

@@ -1,0 +1,298 @@
+// ref_shim.cpp -- extern "C" wrapper over the UNMODIFIED reference headers
+// (/root/reference/proj/include/pixelseg/*.hpp), compiled by oracle/Makefile into
+// oracle/_ref/libpixelseg_ref.so. TEST INFRASTRUCTURE ONLY: it lets tests/golden/make_golden.py
+// produce golden vectors from the reference itself, pins the C restatement
+// (oracle/pixelseg_oracle.c) against the reference, and is the "reference" CPU baseline of
+// bench.py --impl reference. No reference source is copied here; the headers are included
+// from where they lie, with the reference's own build flags (-std=c++20 -O3 -DNDEBUG,
+// proj/CMakeLists.txt:3-10).
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "pixelseg/convert.hpp"
+#include "pixelseg/layers.hpp"
+#include "pixelseg/netgraph.hpp"
+#include "pixelseg/netspec.hpp"
+#include "pixelseg/pipeline.hpp"
+#include "pixelseg/tensor.hpp"
+
+using namespace pixelseg;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guard(F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const SizeError& e) {
+    g_err = e.what();
+    return 6;
+  } catch (const SpecError& e) {
+    g_err = e.what();
+    return 2;
+  } catch (const IoError& e) {
+    g_err = e.what();
+    return 3;
+  } catch (const NumericError& e) {
+    g_err = e.what();
+    return 4;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 9;
+  }
+}
+
+template <typename S>
+Blob<S> make_blob(const S* p, int c, int h, int w) {
+  Blob<S> b(c, h, w);
+  std::memcpy(b.data.data(), p, b.size() * sizeof(S));
+  return b;
+}
+
+struct RefNet {
+  NetSpec spec;
+  NetStates<float> states;
+  std::unique_ptr<NetRunner<float>> runner;
+  Blob<float> last;
+};
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_im2col_f32(const float* in, int C, int H, int W, int k, int d, int s, int p, float* col) {
+  return guard([&] {
+    const Blob<float> b = make_blob(in, C, H, W);
+    const ConvGeometry g = ConvGeometry::from_input(k, d, s, p, H, W);
+    ColumnBuffer<float> cb;
+    im2col_sk(b, g, cb);
+    std::memcpy(col, cb.data.data(), sizeof(float) * cb.rows * cb.cols);
+  });
+}
+
+void ref_gemm_f32(int ta, int tb, int m, int n, int k, float alpha, const float* a, const float* b,
+                  float beta, float* c) {
+  gemm<float>(ta != 0, tb != 0, m, n, k, alpha, a, b, beta, c);
+}
+
+void ref_gemm_f64(int ta, int tb, int m, int n, int k, double alpha, const double* a,
+                  const double* b, double beta, double* c) {
+  gemm<double>(ta != 0, tb != 0, m, n, k, alpha, a, b, beta, c);
+}
+
+#define REF_CONV(NAME, S)                                                                       \
+  int NAME(const S* in, int C, int H, int W, const S* w, const S* bias, int f_out, int k, int d, \
+           int s, int p, S* out) {                                                              \
+    return guard([&] {                                                                          \
+      const Blob<S> b = make_blob(in, C, H, W);                                                 \
+      LayerState<S> st;                                                                         \
+      st.init_conv(f_out, C * k * k);                                                           \
+      std::memcpy(st.weights.data(), w, sizeof(S) * st.weights.size());                         \
+      std::memcpy(st.bias.data(), bias, sizeof(S) * st.bias.size());                            \
+      const ConvGeometry g = ConvGeometry::from_input(k, d, s, p, H, W);                        \
+      ColumnBuffer<S> cb;                                                                       \
+      Blob<S> o;                                                                                \
+      conv_sk_forward(b, st, f_out, g, cb, o);                                                  \
+      std::memcpy(out, o.data.data(), sizeof(S) * o.size());                                    \
+    });                                                                                         \
+  }
+REF_CONV(ref_conv_f32, float)
+REF_CONV(ref_conv_f64, double)
+
+int ref_maxpool_f32(const float* in, int C, int H, int W, int k, int d, int s, float* out,
+                    uint64_t* argmax) {
+  return guard([&] {
+    const Blob<float> b = make_blob(in, C, H, W);
+    const ConvGeometry g = ConvGeometry::from_input(k, d, s, 0, H, W);
+    LayerState<float> st;
+    Blob<float> o;
+    maxpool_sk_forward(b, st, g, o);
+    std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+    if (argmax)
+      for (std::size_t i = 0; i < st.argmax.size(); ++i) argmax[i] = st.argmax[i];
+  });
+}
+
+void ref_relu_f32(const float* in, int C, int H, int W, float* out) {
+  const Blob<float> b = make_blob(in, C, H, W);
+  Blob<float> o;
+  relu_forward(b, o);
+  std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+}
+
+void ref_upconv_f32(const float* in, int C, int H, int W, float* out) {
+  const Blob<float> b = make_blob(in, C, H, W);
+  Blob<float> o;
+  upconv_forward(b, o);
+  std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+}
+
+int ref_mergecrop_f32(const float* a, int Ca, int Ha, int Wa, const float* b, int Cb, int Hb,
+                      int Wb, float* out) {
+  return guard([&] {
+    const Blob<float> A = make_blob(a, Ca, Ha, Wa);
+    const Blob<float> B = make_blob(b, Cb, Hb, Wb);
+    Blob<float> o;
+    mergecrop_forward(A, B, o);
+    std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+  });
+}
+
+void ref_softmax_f32(const float* in, int C, int H, int W, float* out) {
+  const Blob<float> b = make_blob(in, C, H, W);
+  Blob<float> o;
+  softmax_forward(b, o);
+  std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+}
+
+int ref_mirror_pad_u8(const uint8_t* img, int H, int W, int v, uint8_t* out) {
+  return guard([&] {
+    Plane<std::uint8_t> p(H, W);
+    std::memcpy(p.pix.data(), img, p.size());
+    const Plane<std::uint8_t> o = mirror_pad(p, v);
+    std::memcpy(out, o.pix.data(), o.size());
+  });
+}
+
+void ref_normalize_f32(const uint8_t* img, int n, float* out) {
+  Plane<std::uint8_t> p(1, n);
+  std::memcpy(p.pix.data(), img, n);
+  const Plane<float> o = normalize_image<float>(p);
+  std::memcpy(out, o.pix.data(), sizeof(float) * n);
+}
+
+// ---- net-level entry points ----
+void* ref_net_create(const char* text) {
+  RefNet* n = nullptr;
+  const int rc = guard([&] {
+    n = new RefNet;
+    n->spec = parse_netspec_or_throw(text);
+  });
+  if (rc) {
+    delete n;
+    return nullptr;
+  }
+  return n;
+}
+
+void ref_net_destroy(void* h) { delete static_cast<RefNet*>(h); }
+
+// Returns the corrected spec text of a sliding-window net (convert.hpp:175-195) into buf.
+int ref_correct_sw(const char* text, char* buf, int cap) {
+  return guard([&] {
+    const NetSpec s = correct_sw(parse_netspec_or_throw(text));
+    const std::string out = write_netspec(s);
+    if (static_cast<int>(out.size()) + 1 > cap) throw SpecError("buffer too small");
+    std::memcpy(buf, out.c_str(), out.size() + 1);
+  });
+}
+
+int ref_net_init_weights(void* h, uint64_t seed) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    n->states = init_weights<float>(n->spec, seed);
+    n->runner.reset();
+  });
+}
+
+int ref_net_num_layers(void* h) { return static_cast<int>(static_cast<RefNet*>(h)->spec.layers.size()); }
+
+// weights/bias sizes of a layer (0 for parameterless layers)
+void ref_net_param_sizes(void* h, int layer, long long* nw, long long* nb) {
+  RefNet* n = static_cast<RefNet*>(h);
+  *nw = static_cast<long long>(n->states.layers[layer].weights.size());
+  *nb = static_cast<long long>(n->states.layers[layer].bias.size());
+}
+
+void ref_net_get_params(void* h, int layer, float* w, float* b) {
+  RefNet* n = static_cast<RefNet*>(h);
+  const auto& st = n->states.layers[layer];
+  if (w) std::memcpy(w, st.weights.data(), sizeof(float) * st.weights.size());
+  if (b) std::memcpy(b, st.bias.data(), sizeof(float) * st.bias.size());
+}
+
+void ref_net_set_params(void* h, int layer, const float* w, const float* b) {
+  RefNet* n = static_cast<RefNet*>(h);
+  auto& st = n->states.layers[layer];
+  if (w) std::memcpy(st.weights.data(), w, sizeof(float) * st.weights.size());
+  if (b) std::memcpy(st.bias.data(), b, sizeof(float) * st.bias.size());
+}
+
+int ref_net_set_layer_fout(void* h, const char* layer, int f_out, double sigma) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    for (auto& l : n->spec.layers)
+      if (l.name == layer) {
+        l.f_out = f_out;
+        if (l.init != InitKind::None && sigma > 0) l.init_sigma = sigma;
+        return;
+      }
+    throw SpecError("no layer");
+  });
+}
+
+int ref_net_output_extent(void* h, int w0, int* out) {
+  return guard([&] { *out = output_extent(static_cast<RefNet*>(h)->spec, w0); });
+}
+
+long long ref_net_flops(void* h, int w0) {
+  long long t = -1;
+  guard([&] { t = flop_estimate(static_cast<RefNet*>(h)->spec, w0).total; });
+  return t;
+}
+
+// Runs NetRunner<float>::forward (netgraph.hpp:64-84); output shape returned via c/hh/ww.
+int ref_net_forward(void* h, const float* in, int C, int H, int W, int* oc, int* oh, int* ow) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    if (!n->runner) n->runner = std::make_unique<NetRunner<float>>(n->spec, n->states);
+    const Blob<float> b = make_blob(in, C, H, W);
+    n->last = n->runner->forward(b);
+    *oc = n->last.channels;
+    *oh = n->last.height;
+    *ow = n->last.width;
+  });
+}
+
+int ref_net_blob_shape(void* h, const char* name, int* c, int* hh, int* ww) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    if (!n->runner) throw SpecError("no runner");
+    const Blob<float>& b = n->runner->blob(name);
+    *c = b.channels;
+    *hh = b.height;
+    *ww = b.width;
+  });
+}
+
+int ref_net_blob(void* h, const char* name, float* dst) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    if (!n->runner) throw SpecError("no runner");
+    const Blob<float>& b = n->runner->blob(name);
+    std::memcpy(dst, b.data.data(), sizeof(float) * b.size());
+  });
+}
+
+// process<float> (pipeline.hpp:630-698): probs is C x H x W.
+int ref_process(void* h, const uint8_t* img, int H, int W, int w, int v, uint8_t* labels,
+                float* probs) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    Plane<std::uint8_t> p(H, W);
+    std::memcpy(p.pix.data(), img, p.size());
+    const ProcessResult<float> r = process(n->spec, n->states, p, w, v);
+    std::memcpy(labels, r.labels.pix.data(), r.labels.size());
+    for (std::size_t c = 0; c < r.probs.size(); ++c)
+      std::memcpy(probs + c * static_cast<std::size_t>(H) * W, r.probs[c].pix.data(),
+                  sizeof(float) * r.probs[c].size());
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// kernels.cuh -- launchers of the sm_100a kernels (one per reference hot-path function).
+// Activations on the device are stored as f64 holding float values exactly ("widened f32"):
+// the conv's DMMA operands need no per-use conversion, and every non-conv layer's result is
+// still the reference's float result, bit for bit.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace graft {
+
+// Shape of one conv_sk launch over a batch of B images (tiles) of C x H x W.
+struct ConvShape {
+  int B = 1, C = 0, H = 0, W = 0;  // input
+  int M = 0;                       // f_out
+  int k = 1, d = 1, s = 1, p = 0;
+  int OH = 0, OW = 0;
+};
+
+// ---- conv_exact.cu ------------------------------------------------------------------------
+// Device layout of conv weights for the DMMA kernel: f64, K padded to 16 taps, M padded to
+// the 128-row block, tiled as [M/128][K/4][16][32] so one 16-tap chunk of one 128-row block
+// is one contiguous 16 KB run in DMMA A-fragment order (lane = m_local*4 + k_local).
+size_t conv_weight_tiled_elems(int M, int K);
+void tile_conv_weights(const float* w_f32_dev, int M, int K, double* tiled, cudaStream_t st);
+
+// out[b][m][oy][ox] = float(sum_kk w[m][kk]*x[b][kk-tap]) + bias[m], the sum an fp64 fma chain
+// in ascending kk (bit-identical to conv_sk_forward, layers.hpp:43-64). Outputs are nullable:
+// out_f64 = conv blob, out_relu_f64 = relu(conv) (fused relu_forward), out_f32 = conv as f32.
+void conv_exact(const double* in, const double* w_tiled, const float* bias, const ConvShape& sh,
+                double* out_f64, double* out_relu_f64, float* out_f32, cudaStream_t st);
+
+// S=double variant (tests / LayerState<double>): products rounded, mul then add, no FMA,
+// exactly like the reference's x86-64 build. Weights f64 row-major [M][K].
+void conv_f64_muladd(const double* in, const double* w, const double* bias, const ConvShape& sh,
+                     double* out, cudaStream_t st);
+
+// ---- layers.cu ------------------------------------------------------------------------------
+void f32_to_f64(const float* in, double* out, size_t n, cudaStream_t st);
+void f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
+
+// maxpool_sk_forward (layers.hpp:102-132) over B x C planes; argmax nullable (per-image index).
+void maxpool(const double* in, int B, int C, int H, int W, int k, int d, int s, int OH, int OW,
+             double* out, uint64_t* argmax, cudaStream_t st);
+void relu(const double* in, double* out, size_t n, cudaStream_t st);
+void upconv(const double* in, int B, int C, int H, int W, double* out, cudaStream_t st);
+// mergecrop_forward (layers.hpp:196-212) for a batch: out[b] = a[b] ++ crop(b[b]).
+void mergecrop(const double* a, int Ca, int Ha, int Wa, const double* b, int Cb, int Hb, int Wb,
+               int B, double* out, cudaStream_t st);
+// softmax_forward (layers.hpp:227-244); is_double selects S (the subtraction x-m in S).
+void softmax(const double* in, int B, int C, int H, int W, double* out, bool is_double,
+             cudaStream_t st);
+template <typename T>
+void im2col(const T* in, int C, int H, int W, int k, int d, int s, int p, int OH, int OW, T* col,
+            cudaStream_t st);
+template <typename T>
+void gemm(bool ta, bool tb, int m, int n, int k, T alpha, const T* a, const T* b, T beta, T* c,
+          cudaStream_t st);
+void mirror_pad_u8(const uint8_t* img, int H, int W, int v, uint8_t* out, cudaStream_t st);
+void normalize_u8(const uint8_t* img, size_t n, float* out, cudaStream_t st);
+
+// process() pieces (pipeline.hpp:654-694). Tiles are addressed by their row-major index in
+// process()'s tiling: tile i sits at (min((i / ntx) * w, H - w), min((i % ntx) * w, W - w)),
+// which is the edge-snapping tile_offsets lambda (pipeline.hpp:662-672).
+// Builds the inputs of tiles [t0, t0 + n_tiles) as n_tiles x f0 x (w+v) x (w+v) widened f32:
+// mirror_pad + normalize_image + the f0-channel copy, straight from the raw u8 image.
+void build_tiles(const uint8_t* img, int H, int W, int v, int w, int ntx, int t0, int n_tiles,
+                 int f0, double* out, cudaStream_t st);
+// Softmax head + per-pixel argmax + stitch of the tiles' scores (n_tiles x C x w x w) into the
+// image planes: labels H x W (u8), probs C x H x W (f32); rows outside [y_lo, y_hi) skipped.
+void softmax_stitch(const double* scores, int n_tiles, int C, int w, int ntx, int t0, int H, int W,
+                    int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st);
+
+}  // namespace graft

@@ -1,0 +1,203 @@
+"""GPU parity of NetRunner::forward (netgraph.hpp:64-84) and process (pipeline.hpp:630-698):
+every blob bit-identical to the reference's (golden fixtures from oracle/_ref), the full-size
+proj/configs nets checked by per-blob SHA-256 of the reference's own blobs, and the reference's
+tiling invariance checked at sizes the CPU cannot reach. Mirrors proj/tests/test_netgraph.cpp
+and test_pipeline.cpp."""
+import hashlib
+
+import numpy as np
+import pytest
+
+import paper_1509_03371_b200 as g
+from conftest import assert_bitwise, config_text, load_golden
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def spec_of(gnets, key):
+    return g.parse_netspec_or_throw(bytes(gnets[key]).decode())
+
+
+def sk_small():
+    spec = g.parse_netspec_or_throw(config_text("sk.net"))
+    fo = {"conv1": 6, "conv2": 8, "conv3": 12, "ip1": 16, "ip2": 8, "ip3": 2}
+    for l in spec.layers:
+        if l.name in fo:
+            l.f_out = fo[l.name]
+            l.init_sigma = 0.1
+    return spec
+
+
+def test_hand_chained_net(gnets):
+    # proj/tests/test_netgraph.cpp:156-218 (float instantiation): runner == chained layers
+    spec = spec_of(gnets, "chain_spec")
+    states = g.init_weights(spec, 7)
+    runner = g.NetRunner(spec, states)
+    out = runner.forward(g.Blob.from_array(gnets["chain_in"]))
+    assert (out.channels, out.height) == (2, 1)
+    for name in ("conv1", "relu1", "pool1", "conv2", "prob"):
+        assert_bitwise(runner.blob(name).view(), gnets[f"chain_{name}"], name)
+    # chained layer calls on the device agree too
+    x = g.Blob.from_array(gnets["chain_in"])
+    c1, r1, p1, c2, pr = g.Blob(), g.Blob(), g.Blob(), g.Blob(), g.Blob()
+    g.conv_sk_forward(x, states.layers[1], 3, g.ConvGeometry.from_input(3, 1, 1, 0, 8, 8),
+                      g.ColumnBuffer(), c1)
+    g.relu_forward(c1, r1)
+    g.maxpool_sk_forward(r1, states.layers[3], g.ConvGeometry.from_input(2, 1, 2, 0, 6, 6), p1)
+    g.conv_sk_forward(p1, states.layers[4], 2, g.ConvGeometry.from_input(3, 1, 1, 0, 3, 3),
+                      g.ColumnBuffer(), c2)
+    g.softmax_forward(c2, pr)
+    assert_bitwise(pr.data, out.data)
+    w_before = states.layers[1].weights.copy()
+    runner.forward(x)
+    assert np.array_equal(states.layers[1].weights, w_before)
+
+
+def test_runner_errors():
+    # proj/tests/test_netgraph.cpp:220-235
+    spec = g.parse_netspec_or_throw("input w=8 f=2\nlayer c1 conv_sk k=3 fout=2 in=data out=c1\n")
+    states = g.init_weights(spec, 1)
+    runner = g.NetRunner(spec, states)
+    with pytest.raises(g.SizeError, match="3 channels"):
+        runner.forward(g.Blob(3, 8, 8))
+    with pytest.raises(g.SizeError, match="layer 'c1'"):
+        runner.forward(g.Blob(2, 2, 2))
+    with pytest.raises(g.SpecError):
+        runner.blob("nope")
+    with pytest.raises(g.SpecError):
+        g.NetRunner(spec, g.NetStates())
+
+
+def test_u_topology(gnets):
+    # proj/tests/test_netgraph.cpp:238-275
+    spec = spec_of(gnets, "unet_spec")
+    runner = g.NetRunner(spec, g.init_weights(spec, 11))
+    out = runner.forward(g.Blob.from_array(gnets["unet_in"]))
+    assert (out.channels, out.height) == (2, 8)
+    assert runner.blob("merge1").channels == 6 and runner.blob("merge1").height == 10
+    for name in ("conv1", "pool1", "conv2", "upconv1", "merge1", "conv3", "prob"):
+        assert_bitwise(runner.blob(name).view(), gnets[f"unet_{name}"], name)
+
+
+def test_sk_small_resize(gnets):
+    # proj/tests/test_netgraph.cpp:277-308, every blob pinned to the reference's
+    spec = sk_small()
+    runner = g.NetRunner(spec, g.init_weights(spec, 3))
+    out_big = runner.forward(g.Blob.from_array(gnets["sksmall_in"]))
+    assert out_big.height == 9
+    for name in ("conv1", "relu1", "pool1", "conv2", "pool2", "conv3", "pool3", "ip1", "relu4",
+                 "ip2", "ip3", "prob"):
+        assert_bitwise(runner.blob(name).view(), gnets[f"sksmall_{name}"], name)
+    crop = runner.forward(g.Blob.from_array(np.ascontiguousarray(gnets["sksmall_in"][:, :102, :102])))
+    assert_bitwise(crop.view(), gnets["sksmall_crop_prob"], "crop")
+    assert np.abs(crop.view()[:, 0, 0] - out_big.view()[:, 0, 0]).max() <= 1e-5
+
+
+def test_sw_net(gnets):
+    spec = spec_of(gnets, "sw_spec")
+    runner = g.NetRunner(spec, g.init_weights(spec, 1))
+    runner.forward(g.Blob.from_array(gnets["sw_in"]))
+    for name in ("ip1", "ip3", "prob"):
+        assert_bitwise(runner.blob(name).view(), gnets[f"sw_{name}"], name)
+
+
+def test_tiled_process(gnets):
+    # proj/tests/test_pipeline.cpp:535-588
+    spec = spec_of(gnets, "tile_spec")
+    states = g.init_weights(spec, 17)
+    for key, img, w in (("w16", "tile_img", 16), ("w8", "tile_img", 8), ("o13", "tile_odd", 13),
+                        ("o6", "tile_odd", 6)):
+        res = g.process(spec, states, g.Plane.from_array(gnets[img]), w, 5)
+        assert np.array_equal(res.labels.view(), gnets[f"tile_{key}_labels"])
+        probs = np.stack([p.view() for p in res.probs])
+        assert_bitwise(probs, gnets[f"tile_{key}_probs"], key)
+    img = g.Plane.from_array(gnets["tile_img"])
+    with pytest.raises(g.SpecError, match="tile"):
+        g.process(spec, states, img, 16, 4)
+    with pytest.raises(g.SizeError):
+        g.process(spec, states, g.Plane(4, 4), 8, 5)
+
+
+def test_sk_small_process(gnets):
+    spec = sk_small()
+    states = g.init_weights(spec, 3)
+    for w in (9, 16):
+        res = g.process(spec, states, g.Plane.from_array(gnets["skproc_img"]), w, 101)
+        assert np.array_equal(res.labels.view(), gnets[f"skproc_w{w}_labels"])
+        assert_bitwise(np.stack([p.view() for p in res.probs]), gnets[f"skproc_w{w}_probs"])
+
+
+def _full_net(key, cfg, w0):
+    gold = load_golden(f"{key}.npz")
+    spec = g.parse_netspec_or_throw(config_text(cfg))
+    runner = g.NetRunner(spec, g.init_weights(spec, 1))
+    x = g.Rng(1 ^ 0x9e3779b97f4a7c15).uniform_array(3 * w0 * w0, -1.0, 1.0).reshape(3, w0, w0)
+    assert hashlib.sha256(x.tobytes()).hexdigest() == bytes(gold["in_sha"]).decode()
+    runner.forward(g.Blob.from_array(x))
+    bad = []
+    for l in spec.layers[1:]:
+        b = runner.blob(l.output).view()
+        assert tuple(b.shape) == tuple(gold[f"shape_{l.output}"])
+        if hashlib.sha256(np.ascontiguousarray(b).tobytes()).hexdigest() != \
+                bytes(gold[f"sha_{l.output}"]).decode():
+            idx = gold[f"sampidx_{l.output}"]
+            nd = int((b.ravel()[idx].view(np.uint32) != gold[f"sampval_{l.output}"].view(np.uint32)).sum())
+            bad.append(f"{l.output} (sampled mismatches {nd}/{idx.size})")
+    last = spec.layers[-1]
+    assert_bitwise(runner.blob(last.inputs[0]).view(), gold["scores"], "scores")
+    assert_bitwise(runner.blob(last.output).view(), gold["prob"], "prob")
+    assert not bad, "blobs differing from the reference: " + ", ".join(bad)
+
+
+def test_full_sk_net_229():
+    # the paper's headline workload: sk.net at 229 -> 128x128 labels, pixelseg bench --seed 1
+    _full_net("sk229", "sk.net", 229)
+
+
+def test_full_u_net_572():
+    _full_net("u572", "u.net", 572)
+
+
+def test_full_usk_net_692():
+    _full_net("usk692", "usk.net", 692)
+
+
+def test_process_tiling_invariance_full_sk():
+    # beyond the CPU's reach: a 512x384 image through full sk.net with 128-, 200- and
+    # 256-pixel tiles must agree bit for bit (the reference's tiling guarantee), and every
+    # band of a 3-way row partition must equal the whole-image result.
+    spec = g.parse_netspec_or_throw(config_text("sk.net"))
+    states = g.init_weights(spec, 1)
+    img = g.Rng(55).index_array_u8(512 * 384, 256).reshape(512, 384)
+    proc = g.Processor(spec, states)
+    lab128, pr128 = proc.run(img, 128, 101)
+    for w in (200, 256):
+        lab, pr = proc.run(img, w, 101)
+        assert np.array_equal(lab, lab128)
+        assert_bitwise(pr, pr128, f"tile {w}")
+    n = g.tile_rows(512, 128)
+    cuts = [0, 1, 3, n]
+    lab = np.zeros_like(lab128)
+    pr = np.zeros_like(pr128)
+    for r0, r1 in zip(cuts[:-1], cuts[1:]):
+        y0, y1 = g.band_rows(512, 128, r0, r1)
+        lb, pb = proc.run(img, 128, 101, rows=(r0, r1))
+        lab[y0:y1], pr[:, y0:y1] = lb[y0:y1], pb[:, y0:y1]
+    assert np.array_equal(lab, lab128)
+    assert_bitwise(pr, pr128, "bands")
+    # labels are the argmax of the probabilities; probabilities sum to ~1
+    assert np.array_equal(lab, (pr128[1] > pr128[0]).astype(np.uint8))
+    assert np.abs(pr128.astype(np.float64).sum(0) - 1.0).max() < 1e-6
+
+
+def test_process_single_tile_equals_forward():
+    # process() of an image exactly one tile large == NetRunner::forward of its padded input
+    spec = g.parse_netspec_or_throw(config_text("sk.net"))
+    states = g.init_weights(spec, 1)
+    img = g.Rng(9).index_array_u8(128 * 128, 256).reshape(128, 128)
+    res = g.process(spec, states, g.Plane.from_array(img), 128, 101)
+    padded = g.normalize_image(g.mirror_pad(g.Plane.from_array(img), 101)).view()
+    x = np.ascontiguousarray(np.broadcast_to(padded, (3, 229, 229)))
+    out = g.NetRunner(spec, states).forward(g.Blob.from_array(x)).view()
+    assert_bitwise(np.stack([p.view() for p in res.probs]), out, "process vs forward")
