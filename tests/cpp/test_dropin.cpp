@@ -1,0 +1,182 @@
+// test_dropin.cpp -- the C++ drop-in (include/pixelseg_gpu.hpp) against the reference itself,
+// both compiled into one binary: every check compares pixelseg::gpu::X with pixelseg::X on the
+// same inputs, bit for bit. Built by __graft_entry__.build() where /root/reference exists (the
+// reference headers are compile-time only); run on the B200 by tests/test_gpu_dropin_cpp.py.
+// Cases follow proj/tests/test_layers.cpp, test_netgraph.cpp and test_pipeline.cpp.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pixelseg_gpu.hpp"
+
+using namespace pixelseg;
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond, what)                                               \
+  do {                                                                  \
+    if (cond) {                                                         \
+      ++g_pass;                                                         \
+    } else {                                                            \
+      ++g_fail;                                                         \
+      std::printf("FAIL %s (%s:%d)\n", what, __FILE__, __LINE__);       \
+    }                                                                   \
+  } while (0)
+
+template <typename T>
+static bool same_bits(const std::vector<T>& a, const std::vector<T>& b) {
+  return a.size() == b.size() && std::memcmp(a.data(), b.data(), a.size() * sizeof(T)) == 0;
+}
+
+template <typename S>
+static void fill(std::vector<S>& v, Rng& r) {
+  for (auto& x : v) x = static_cast<S>(r.uniform(-1.0, 1.0));
+}
+
+template <typename S>
+static void conv_cases() {
+  Rng rng(5);
+  struct Case { int f_in, f_out, h, w, k, d, s, p; };
+  const Case cases[] = {{3, 4, 9, 9, 3, 1, 1, 0}, {2, 5, 11, 11, 3, 2, 1, 0}, {4, 2, 8, 8, 2, 1, 2, 0},
+                        {1, 3, 7, 7, 7, 1, 1, 0}, {2, 2, 6, 6, 3, 1, 1, 1}, {12, 130, 40, 40, 10, 3, 1, 0}};
+  for (const auto& c : cases) {
+    Blob<S> in(c.f_in, c.h, c.w);
+    fill(in.data, rng);
+    LayerState<S> st;
+    st.init_conv(c.f_out, c.f_in * c.k * c.k);
+    fill(st.weights, rng);
+    fill(st.bias, rng);
+    const ConvGeometry g = ConvGeometry::from_input(c.k, c.d, c.s, c.p, c.h, c.w);
+    ColumnBuffer<S> cb;
+    Blob<S> ref, got;
+    conv_sk_forward(in, st, c.f_out, g, cb, ref);
+    gpu::conv_sk_forward(in, st, c.f_out, g, cb, got);
+    CHECK(same_bits(ref.data, got.data), "conv_sk_forward");
+    CHECK(got.channels == ref.channels && got.height == ref.height, "conv shape");
+  }
+}
+
+static void layer_cases() {
+  Rng rng(11);
+  for (int t = 0; t < 3; ++t) {
+    const int k = 2, d = t + 1, s = t == 0 ? 2 : 1, hw = 9 + 2 * t;
+    Blob<float> in(3, hw, hw);
+    fill(in.data, rng);
+    const ConvGeometry g = ConvGeometry::from_input(k, d, s, 0, hw, hw);
+    LayerState<float> s1, s2;
+    Blob<float> a, b;
+    maxpool_sk_forward(in, s1, g, a);
+    gpu::maxpool_sk_forward(in, s2, g, b);
+    CHECK(same_bits(a.data, b.data) && s1.argmax == s2.argmax, "maxpool_sk_forward");
+    relu_forward(in, a);
+    gpu::relu_forward(in, b);
+    CHECK(same_bits(a.data, b.data), "relu_forward");
+    upconv_forward(in, a);
+    gpu::upconv_forward(in, b);
+    CHECK(same_bits(a.data, b.data), "upconv_forward");
+    softmax_forward(in, a);
+    gpu::softmax_forward(in, b);
+    CHECK(same_bits(a.data, b.data), "softmax_forward");
+    Blob<float> small(2, hw - 3, hw - 4);
+    fill(small.data, rng);
+    mergecrop_forward(small, in, a);
+    gpu::mergecrop_forward(small, in, b);
+    CHECK(same_bits(a.data, b.data), "mergecrop_forward");
+    ColumnBuffer<float> c1, c2;
+    const ConvGeometry gc = ConvGeometry::from_input(3, d, 1, 1, hw, hw);
+    im2col_sk(in, gc, c1);
+    gpu::im2col_sk(in, gc, c2);
+    c1.data.resize(static_cast<std::size_t>(c1.rows) * c1.cols);
+    c2.data.resize(static_cast<std::size_t>(c2.rows) * c2.cols);
+    CHECK(same_bits(c1.data, c2.data), "im2col_sk");
+  }
+  // gemm, all transposes, alpha/beta
+  const int m = 7, n = 9, kk = 13;
+  std::vector<float> A(m * kk), B(kk * n), C0(m * n);
+  fill(A, rng);
+  fill(B, rng);
+  fill(C0, rng);
+  for (int ta = 0; ta < 2; ++ta)
+    for (int tb = 0; tb < 2; ++tb) {
+      std::vector<float> c1 = C0, c2 = C0;
+      gemm<float>(ta, tb, m, n, kk, 0.5f, A.data(), B.data(), 1.5f, c1.data());
+      gpu::gemm<float>(ta, tb, m, n, kk, 0.5f, A.data(), B.data(), 1.5f, c2.data());
+      CHECK(same_bits(c1, c2), "gemm");
+    }
+  // errors: same types and messages
+  LayerState<float> st;
+  st.init_conv(3, 2 * 9);
+  ColumnBuffer<float> cb;
+  Blob<float> in(2, 5, 5), out;
+  std::string e1, e2;
+  try { conv_sk_forward(in, st, 3, ConvGeometry::from_input(5, 1, 1, 0, 5, 5), cb, out); } catch (const SizeError& e) { e1 = e.what(); }
+  try { gpu::conv_sk_forward(in, st, 3, ConvGeometry::from_input(5, 1, 1, 0, 5, 5), cb, out); } catch (const SizeError& e) { e2 = e.what(); }
+  CHECK(!e1.empty() && e1 == e2, "conv weight-count error");
+}
+
+static void net_cases() {
+  const NetSpec spec = parse_netspec_or_throw(
+      "input w=8 f=2\n"
+      "layer conv1 conv_sk k=3 fout=3 in=data out=conv1 init=gaussian:0.5\n"
+      "layer relu1 relu in=conv1 out=relu1\n"
+      "layer pool1 pool_max k=2 s=2 in=relu1 out=pool1\n"
+      "layer conv2 conv_sk k=3 fout=2 in=pool1 out=conv2 init=gaussian:0.5\n"
+      "layer prob softmax_loss in=conv2 out=prob\n");
+  auto states = init_weights<float>(spec, 7);
+  Blob<float> input(2, 8, 8);
+  Rng rng(99);
+  fill(input.data, rng);
+  NetRunner<float> ref(spec, states);
+  gpu::NetRunner<float> got(spec, states);
+  const Blob<float> r = ref.forward(input);
+  const Blob<float> g = got.forward(input);
+  CHECK(same_bits(r.data, g.data), "NetRunner::forward");
+  for (const char* name : {"conv1", "relu1", "pool1", "conv2"})
+    CHECK(same_bits(ref.blob(name).data, got.blob(name).data), name);
+  // weights change between calls -> the drop-in re-uploads
+  states.layers[1].weights[0] += 0.25f;
+  CHECK(same_bits(ref.forward(input).data, got.forward(input).data), "forward after weight change");
+  std::string e1, e2;
+  try { ref.forward(Blob<float>(3, 8, 8)); } catch (const SizeError& e) { e1 = e.what(); }
+  try { got.forward(Blob<float>(3, 8, 8)); } catch (const SizeError& e) { e2 = e.what(); }
+  CHECK(!e1.empty() && e1 == e2, "forward channel error");
+  try { ref.forward(Blob<float>(2, 2, 2)); } catch (const SizeError& e) { e1 = e.what(); }
+  try { got.forward(Blob<float>(2, 2, 2)); } catch (const SizeError& e) { e2 = e.what(); }
+  CHECK(e1 == e2, "forward layer error");
+}
+
+static void process_cases() {
+  const NetSpec spec = parse_netspec_or_throw(
+      "input w=21 f=1\n"
+      "layer c1 conv_sk k=3 fout=4 in=data out=c1 init=he\n"
+      "layer r1 relu in=c1 out=r1\n"
+      "layer p1 pool_max k=2 s=1 in=r1 out=p1\n"
+      "layer c2 conv_sk k=2 d=2 fout=3 in=p1 out=c2 init=he\n"
+      "layer prob softmax_loss in=c2 out=prob\n");
+  NetStates<float> states = init_weights<float>(spec, 17);
+  Rng rng(55);
+  Plane<std::uint8_t> img(37, 29);
+  for (auto& p : img.pix) p = static_cast<std::uint8_t>(rng.uniform_index(256));
+  for (int w : {16, 8, 5}) {
+    const ProcessResult<float> a = process(spec, states, img, w, 5);
+    const ProcessResult<float> b = gpu::process(spec, states, img, w, 5);
+    CHECK(a.labels.pix == b.labels.pix, "process labels");
+    bool ok = a.probs.size() == b.probs.size();
+    for (std::size_t c = 0; ok && c < a.probs.size(); ++c) ok = same_bits(a.probs[c].pix, b.probs[c].pix);
+    CHECK(ok, "process probs");
+  }
+  std::string e1, e2;
+  try { process(spec, states, img, 16, 4); } catch (const SpecError& e) { e1 = e.what(); }
+  try { gpu::process(spec, states, img, 16, 4); } catch (const SpecError& e) { e2 = e.what(); }
+  CHECK(!e1.empty() && e1 == e2, "process tile error");
+}
+
+int main() {
+  conv_cases<float>();
+  conv_cases<double>();
+  layer_cases();
+  net_cases();
+  process_cases();
+  std::printf("drop-in vs reference: %d passed, %d failed\n", g_pass, g_fail);
+  return g_fail ? 1 : 0;
+}
