@@ -449,7 +449,7 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--tile", type=int, default=128)
     ap.add_argument("--tile-batch", type=int, default=0)
-    ap.add_argument("--cpu-tile", type=int, default=4, help="labels per side of a CPU sample tile")
+    ap.add_argument("--cpu-tile", type=int, default=8, help="labels per side of a CPU sample tile")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()

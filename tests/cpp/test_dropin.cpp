@@ -59,7 +59,7 @@ static void conv_cases() {
 static void layer_cases() {
   Rng rng(11);
   for (int t = 0; t < 3; ++t) {
-    const int k = 2, d = t + 1, s = t == 0 ? 2 : 1, hw = 9 + 2 * t;
+    const int k = 2, d = t + 1, s = t == 0 ? 2 : 1, hw = 10 + t;
     Blob<float> in(3, hw, hw);
     fill(in.data, rng);
     const ConvGeometry g = ConvGeometry::from_input(k, d, s, 0, hw, hw);
