@@ -50,6 +50,7 @@ struct ConvArgs {
   long long N;    // B*OH*OW output pixels
   long long CHW;  // per-image input stride
   int C, H, W, M, K, k, d, s, p, OH, OW, OHW, kk2;
+  int iwp, owp;  // row pitches (doubles) of the input and output blobs
   int MG;       // padded M / 8 (row groups per k-group in the weight layout)
   unsigned mblocks;
   // exact division of a tap index (< 2^24) by k*k and by k: q = (n * mul) >> sh
@@ -138,11 +139,11 @@ __global__ void __launch_bounds__(NTHREADS, MINB) conv_exact_kernel(const ConvAr
     const int ox = rem - oy * a.OW;
     iy0[h] = oy * a.s - a.p;
     ix0[h] = ox * a.s - a.p;
-    pix_base[h] = static_cast<long long>(b) * a.CHW + static_cast<long long>(iy0[h]) * a.W + ix0[h];
+    pix_base[h] = static_cast<long long>(b) * a.CHW + static_cast<long long>(iy0[h]) * a.iwp + ix0[h];
   }
   const double* wblk = a.wt + static_cast<size_t>(mb) * BM * 4;  // row-group offset in a k-group
   const size_t kg_stride = static_cast<size_t>(a.MG) * 32;       // doubles per k-group
-  const long long HW = static_cast<long long>(a.H) * a.W;
+  const long long HW = static_cast<long long>(a.H) * a.iwp;
 
   auto load_chunk = [&](int chunk, int stage) {
     double* adst = As + stage * A_ELEMS;
@@ -164,7 +165,7 @@ __global__ void __launch_bounds__(NTHREADS, MINB) conv_exact_kernel(const ConvAr
       const int ky = fast_div(r, a.mul_k, a.sh_k);
       const int kx = r - ky * a.k;
       const int dy = ky * a.d, dx = kx * a.d;
-      const long long toff = c * HW + static_cast<long long>(dy) * a.W + dx;
+      const long long toff = c * HW + static_cast<long long>(dy) * a.iwp + dx;
 #pragma unroll
       for (int h = 0; h < NPIX; ++h) {
         const int iy = iy0[h] + dy, ix = ix0[h] + dx;
@@ -224,12 +225,14 @@ __global__ void __launch_bounds__(NTHREADS, MINB) conv_exact_kernel(const ConvAr
       const long long n = n0 + (wn * TN + i) * 8 + 2 * (lane & 3) + e;
       if (n >= a.N) continue;
       const long long b = n / a.OHW;
-      const long long rem = n - b * a.OHW;
+      const int rem = static_cast<int>(n - b * a.OHW);
+      const int oy = rem / a.OW;
+      const long long opix = static_cast<long long>(oy) * a.owp + (rem - oy * a.OW);
 #pragma unroll
       for (int j = 0; j < TM; ++j) {
         const int m = mb * BM + (wm * TM + j) * 8 + (lane >> 2);
         if (m >= a.M) continue;
-        const long long idx = (b * a.M + m) * a.OHW + rem;
+        const long long idx = (b * a.M + m) * static_cast<long long>(a.OH) * a.owp + opix;
         const float v = __fadd_rn(__double2float_rn(acc[j][i][e]), a.bias[m]);
         if (a.out) a.out[idx] = static_cast<double>(v);
         if (a.out_relu) a.out_relu[idx] = v > 0.0f ? static_cast<double>(v) : 0.0;
@@ -326,11 +329,11 @@ __global__ void __launch_bounds__(32 * (WM * WN + NPROD), MINB) conv_ws_kernel(c
       const int ox = rem - oy * a.OW;
       iy0[h] = oy * a.s - a.p;
       ix0[h] = ox * a.s - a.p;
-      pix_base[h] = static_cast<long long>(b) * a.CHW + static_cast<long long>(iy0[h]) * a.W + ix0[h];
+      pix_base[h] = static_cast<long long>(b) * a.CHW + static_cast<long long>(iy0[h]) * a.iwp + ix0[h];
     }
     const double* wblk = a.wt + static_cast<size_t>(mb) * BM * 4;
     const size_t kg_stride = static_cast<size_t>(a.MG) * 32;
-    const long long HW = static_cast<long long>(a.H) * a.W;
+    const long long HW = static_cast<long long>(a.H) * a.iwp;
     for (int chunk = 0; chunk < nchunks; ++chunk) {
       const int stage = chunk % STAGES;
       if (chunk >= STAGES) mbar_wait(&empty[stage], ((chunk / STAGES) - 1) & 1);
@@ -353,7 +356,7 @@ __global__ void __launch_bounds__(32 * (WM * WN + NPROD), MINB) conv_ws_kernel(c
         const int ky = fast_div(r, a.mul_k, a.sh_k);
         const int kx = r - ky * a.k;
         const int dy = ky * a.d, dx = kx * a.d;
-        const long long toff = c * HW + static_cast<long long>(dy) * a.W + dx;
+        const long long toff = c * HW + static_cast<long long>(dy) * a.iwp + dx;
 #pragma unroll
         for (int h = 0; h < NPIX; ++h) {
           const int iy = iy0[h] + dy, ix = ix0[h] + dx;
@@ -404,12 +407,14 @@ __global__ void __launch_bounds__(32 * (WM * WN + NPROD), MINB) conv_ws_kernel(c
       const long long n = n0 + (wn * TN + i) * 8 + 2 * (lane & 3) + e;
       if (n >= a.N) continue;
       const long long b = n / a.OHW;
-      const long long rem = n - b * a.OHW;
+      const int rem = static_cast<int>(n - b * a.OHW);
+      const int oy = rem / a.OW;
+      const long long opix = static_cast<long long>(oy) * a.owp + (rem - oy * a.OW);
 #pragma unroll
       for (int j = 0; j < TM; ++j) {
         const int m = mb * BM + (wm * TM + j) * 8 + (lane >> 2);
         if (m >= a.M) continue;
-        const long long idx = (b * a.M + m) * a.OHW + rem;
+        const long long idx = (b * a.M + m) * static_cast<long long>(a.OH) * a.owp + opix;
         const float v = __fadd_rn(__double2float_rn(acc[j][i][e]), a.bias[m]);
         if (a.out) a.out[idx] = static_cast<double>(v);
         if (a.out_relu) a.out_relu[idx] = v > 0.0f ? static_cast<double>(v) : 0.0;
@@ -508,10 +513,7 @@ int pick_variant(int M) {
     return e ? std::atoi(e) : -1;
   }();
   if (forced >= 0) return forced;
-  // measured on B200 (profiles/r01_conv_variants.md): warp-specialized kernels win; 64-row
-  // blocks when f_out does not fill 128-row blocks
-  if (M <= 64 || M % 128 != 0) return 9;
-  return 12;
+  return -1;
 }
 
 }  // namespace
@@ -558,10 +560,18 @@ void conv_exact(const double* in, const double* w_tiled, const float* bias, cons
   magic_div(a.k, &a.mul_k, &a.sh_k);
   if (a.K >= (1 << 24) || a.kk2 >= (1 << 16)) throw_arg("conv: fan-in too large");
   a.MG = (a.M + MPAD - 1) / MPAD * MPAD / 8;
+  a.iwp = sh.in_wp ? sh.in_wp : sh.W;
+  a.owp = sh.out_wp ? sh.out_wp : sh.OW;
   a.N = static_cast<long long>(sh.B) * a.OHW;
-  a.CHW = static_cast<long long>(sh.C) * sh.H * sh.W;
+  a.CHW = static_cast<long long>(sh.C) * sh.H * a.iwp;
   if (a.N == 0 || a.M == 0) return;
-  switch (pick_variant(a.M)) {
+  if (pick_variant(a.M) == 100 || (pick_variant(a.M) < 0 && conv_tma_eligible(sh))) {
+    conv_tma(in, w_tiled, bias, sh, out_f64, out_relu_f64, out_f32, st);
+    return;
+  }
+  int v = pick_variant(a.M);
+  if (v < 0) v = (a.M <= 64 || a.M % 128 != 0) ? 9 : 12;  // cp.async path (s > 1, odd pitch)
+  switch (v) {
     case 0: launch_variant<128, 128, 16, 2, 4, 3, 1>(a, st); break;  // r01: 64x32 warp tiles
     case 2: launch_variant<64, 128, 16, 2, 4, 4, 2>(a, st); break;   // 32x32 warp tiles
     case 3: launch_variant<128, 64, 32, 4, 2, 2, 2>(a, st); break;   // BK 32, double buffer

@@ -17,6 +17,7 @@ struct ConvShape {
   int M = 0;                       // f_out
   int k = 1, d = 1, s = 1, p = 0;
   int OH = 0, OW = 0;
+  int in_wp = 0, out_wp = 0;       // row pitches in doubles (0 = compact)
 };
 
 // ---- conv_exact.cu ------------------------------------------------------------------------
@@ -32,6 +33,12 @@ void tile_conv_weights(const float* w_f32_dev, int M, int K, double* tiled, cuda
 void conv_exact(const double* in, const double* w_tiled, const float* bias, const ConvShape& sh,
                 double* out_f64, double* out_relu_f64, float* out_f32, cudaStream_t st);
 
+// TMA-fed variant (conv_tma.cu) used by conv_exact for stride-1 layers with 16-byte row
+// pitches (every net blob); same arithmetic, same results.
+bool conv_tma_eligible(const ConvShape& sh);
+void conv_tma(const double* in, const double* w_tiled, const float* bias, const ConvShape& sh,
+              double* out_f64, double* out_relu_f64, float* out_f32, cudaStream_t st);
+
 // S=double variant (tests / LayerState<double>): products rounded, mul then add, no FMA,
 // exactly like the reference's x86-64 build. Weights f64 row-major [M][K].
 void conv_f64_muladd(const double* in, const double* w, const double* bias, const ConvShape& sh,
@@ -42,16 +49,22 @@ void f32_to_f64(const float* in, double* out, size_t n, cudaStream_t st);
 void f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
 
 // maxpool_sk_forward (layers.hpp:102-132) over B x C planes; argmax nullable (per-image index).
+// Row pitches (wp*, in doubles) default to compact rows when 0.
+void f32_to_f64_pitched(const float* in, long long rows, int W, int wp, double* out,
+                        cudaStream_t st);
+void f64_pitched_to_f32(const double* in, long long rows, int W, int wp, float* out,
+                        cudaStream_t st);
 void maxpool(const double* in, int B, int C, int H, int W, int k, int d, int s, int OH, int OW,
-             double* out, uint64_t* argmax, cudaStream_t st);
+             double* out, uint64_t* argmax, cudaStream_t st, int wpi = 0, int wpo = 0);
 void relu(const double* in, double* out, size_t n, cudaStream_t st);
-void upconv(const double* in, int B, int C, int H, int W, double* out, cudaStream_t st);
+void upconv(const double* in, int B, int C, int H, int W, double* out, cudaStream_t st,
+            int wpi = 0, int wpo = 0);
 // mergecrop_forward (layers.hpp:196-212) for a batch: out[b] = a[b] ++ crop(b[b]).
 void mergecrop(const double* a, int Ca, int Ha, int Wa, const double* b, int Cb, int Hb, int Wb,
-               int B, double* out, cudaStream_t st);
+               int B, double* out, cudaStream_t st, int wpa = 0, int wpb = 0, int wpo = 0);
 // softmax_forward (layers.hpp:227-244); is_double selects S (the subtraction x-m in S).
 void softmax(const double* in, int B, int C, int H, int W, double* out, bool is_double,
-             cudaStream_t st);
+             cudaStream_t st, int wp = 0);
 template <typename T>
 void im2col(const T* in, int C, int H, int W, int k, int d, int s, int p, int OH, int OW, T* col,
             cudaStream_t st);
@@ -67,10 +80,10 @@ void normalize_u8(const uint8_t* img, size_t n, float* out, cudaStream_t st);
 // Builds the inputs of tiles [t0, t0 + n_tiles) as n_tiles x f0 x (w+v) x (w+v) widened f32:
 // mirror_pad + normalize_image + the f0-channel copy, straight from the raw u8 image.
 void build_tiles(const uint8_t* img, int H, int W, int v, int w, int ntx, int t0, int n_tiles,
-                 int f0, double* out, cudaStream_t st);
+                 int f0, double* out, cudaStream_t st, int wp = 0);
 // Softmax head + per-pixel argmax + stitch of the tiles' scores (n_tiles x C x w x w) into the
 // image planes: labels H x W (u8), probs C x H x W (f32); rows outside [y_lo, y_hi) skipped.
 void softmax_stitch(const double* scores, int n_tiles, int C, int w, int ntx, int t0, int H, int W,
-                    int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st);
+                    int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st, int wp = 0);
 
 }  // namespace graft
