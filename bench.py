@@ -238,7 +238,7 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = g.parse_netspec_or_throw(sk_text())
     states = g.init_weights(spec, 1)
-    proc = g.Processor(spec, states, tile_batch=args.tile_batch)
+    proc = g.Processor(spec, states, tile_batch=args.tile_batch, retile=args.retile)
     net = proc.net.h
     C = proc.n_classes
     H = W = args.size
@@ -378,8 +378,9 @@ def run_ours(args):
     # ---- roofline of the dominant kernel (ip1's conv_exact launches) ----
     names = [l.name for l in spec.layers]
     ip1 = names.index("ip1")
-    fl = g.flop_estimate(spec, w + V)
-    n_tiles = g.tile_rows(H, w) * g.tile_rows(W, w)
+    wi = proc.last_tile()  # internal tile process() chose (bit-identical planes for any tile)
+    fl = g.flop_estimate(spec, wi + V)
+    n_tiles = ((H + wi - 1) // wi) * ((W + wi - 1) // wi)
     ip1_flops_total = fl["ip1"] * n_tiles * args.steps
     ip1_ms = ms[ip1]
     achieved = ip1_flops_total / (ip1_ms * 1e-3) / 1e12 if ip1_ms > 0 else None
@@ -401,8 +402,9 @@ def run_ours(args):
         "unit": "TFLOP/s",
         "frac": achieved / peak_sustained if achieved else None,
         "traffic": traffic,
-        "kernel": "conv_exact_kernel (ip1: M=1024, K=19200, 16384 px/tile)",
+        "kernel": f"conv_tma_kernel (ip1: M=1024, K=19200, {wi * wi} px per internal tile)",
         "flops_per_launch": fl["ip1"] * n_tiles * args.steps / max(1, runs[ip1]),
+        "flops_source": "flop_estimate(sk.net, internal tile + 101), convert.hpp:308-322",
         "avg_launch_ms": ip1_ms / max(1, runs[ip1]),
         "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
         "conv_share_of_step": conv_ms / all_ms if all_ms else None,
@@ -421,7 +423,9 @@ def run_ours(args):
         "vs_baseline": value / PUBLISHED_SK_LABELS_PER_S,
         "dtype": "f64",
         "data": "synthetic: Rng(55+rank) u8 image per GPU; weights init_weights(sk.net, seed 1)",
-        "config": workload_config(args, ws),
+        "config": dict(workload_config(args, ws), internal_tile=wi,
+                       flop_per_label=fl["total"] * n_tiles / (H * W),
+                       flop_per_label_reference_tiling=g.flop_estimate(spec, w + V)["total"] / (w * w)),
         "e2e": {"value": e2e_value, "unit": "labels/s", "h2d_bytes_per_step": ws * H * W,
                 "d2h_bytes_per_step": ws * H * W * (1 + 4 * C)},
         "gpu_launches": int(launches),
@@ -449,6 +453,8 @@ def main():
     ap.add_argument("--size", type=int, default=1024)
     ap.add_argument("--tile", type=int, default=128)
     ap.add_argument("--tile-batch", type=int, default=0)
+    ap.add_argument("--retile", type=int, default=1024,
+                    help="largest internal process() tile (0: exactly --tile)")
     ap.add_argument("--cpu-tile", type=int, default=8, help="labels per side of a CPU sample tile")
     ap.add_argument("--cpu-threads", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")

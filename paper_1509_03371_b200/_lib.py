@@ -32,6 +32,8 @@ INIT_NONE, INIT_GAUSSIAN, INIT_HE = range(3)
 OPT_TIMED = 1
 OPT_TILE_BATCH = 2
 OPT_KEEP_BLOBS = 3
+OPT_RETILE = 5
+OPT_LAST_TILE = 6
 
 
 class CudaError(Error):
@@ -111,6 +113,7 @@ _SIGS = {
     "graft_tile_rows": (_i, [_i, _i, _pi]),
     "graft_band_rows": (_i, [_i, _i, _i, _i, _pi, _pi]),
     "graft_net_set_option": (_i, [_vp, _i, C.c_longlong]),
+    "graft_net_get_option": (_i, [_vp, _i, C.POINTER(C.c_longlong)]),
     "graft_rng_create": (_i, [_u64, C.POINTER(_vp)]),
     "graft_rng_destroy": (None, [_vp]),
     "graft_rng_fill_gaussian_f32": (_i, [_vp, _vp, _sz, _d, _d]),

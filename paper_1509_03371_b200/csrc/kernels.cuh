@@ -75,15 +75,16 @@ void mirror_pad_u8(const uint8_t* img, int H, int W, int v, uint8_t* out, cudaSt
 void normalize_u8(const uint8_t* img, size_t n, float* out, cudaStream_t st);
 
 // process() pieces (pipeline.hpp:654-694). Tiles are addressed by their row-major index in
-// process()'s tiling: tile i sits at (min((i / ntx) * w, H - w), min((i % ntx) * w, W - w)),
-// which is the edge-snapping tile_offsets lambda (pipeline.hpp:662-672).
+// process()'s tiling: tile i sits at (min(y_base + (i / ntx) * w, H - w), min((i % ntx) * w,
+// W - w)), the edge-snapping tile_offsets lambda (pipeline.hpp:662-672) started at y_base.
 // Builds the inputs of tiles [t0, t0 + n_tiles) as n_tiles x f0 x (w+v) x (w+v) widened f32:
 // mirror_pad + normalize_image + the f0-channel copy, straight from the raw u8 image.
 void build_tiles(const uint8_t* img, int H, int W, int v, int w, int ntx, int t0, int n_tiles,
-                 int f0, double* out, cudaStream_t st, int wp = 0);
+                 int f0, double* out, cudaStream_t st, int wp = 0, int y_base = 0);
 // Softmax head + per-pixel argmax + stitch of the tiles' scores (n_tiles x C x w x w) into the
 // image planes: labels H x W (u8), probs C x H x W (f32); rows outside [y_lo, y_hi) skipped.
 void softmax_stitch(const double* scores, int n_tiles, int C, int w, int ntx, int t0, int H, int W,
-                    int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st, int wp = 0);
+                    int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st, int wp = 0,
+                    int y_base = 0);
 
 }  // namespace graft

@@ -66,13 +66,18 @@ def validate_process(spec: NetSpec, H: int, W: int, w: int, v: int) -> None:
 class Processor:
     """A device-resident net for repeated process() calls (one upload of the weights)."""
 
-    def __init__(self, spec: NetSpec, states: NetStates, tile_batch: int = 0):
+    def __init__(self, spec: NetSpec, states: NetStates, tile_batch: int = 0,
+                 retile: Optional[int] = None):
+        """retile: largest internal tile process() may use (default 1024; 0 = exactly the
+        caller's w). Every tiling gives bit-identical planes."""
         self.spec = spec
         self.states = states
         self.net = DeviceNet(spec)
         self.net.sync_params(spec, states)
         if tile_batch:
             self.net.set_option(_lib.OPT_TILE_BATCH, tile_batch)
+        if retile is not None:
+            self.net.set_option(_lib.OPT_RETILE, retile)
         self.n_classes = compute_channels(spec)[spec.layers[-1].output]
 
     def run(self, image: np.ndarray, w: int, v: int, labels: Optional[np.ndarray] = None,
@@ -97,6 +102,14 @@ class Processor:
                                                      rows[0], rows[1], _lib.ptr(labels),
                                                      _lib.ptr(probs), mem))
         return labels, probs
+
+
+    def last_tile(self) -> int:
+        """Internal tile size the last run() used."""
+        import ctypes as C
+        v = C.c_longlong()
+        _lib.check(_lib.lib().graft_net_get_option(self.net.h, _lib.OPT_LAST_TILE, C.byref(v)))
+        return v.value
 
 
 def process(spec: NetSpec, states: NetStates, image: Plane, w: int, v: int) -> ProcessResult:

@@ -164,20 +164,29 @@ def test_full_usk_net_692():
 
 
 def test_process_tiling_invariance_full_sk():
-    # beyond the CPU's reach: a 512x384 image through full sk.net with 128-, 200- and
-    # 256-pixel tiles must agree bit for bit (the reference's tiling guarantee), and every
-    # band of a 3-way row partition must equal the whole-image result.
+    # beyond the CPU's reach: a 512x512 image through full sk.net with 128-, 200- and
+    # 256-pixel tiles must agree bit for bit (the reference's tiling guarantee), the internal
+    # retiling (one 512 tile: 2.3% fewer FLOPs) too, and every band of a 3-way row partition
+    # must equal the whole-image result.
     spec = g.parse_netspec_or_throw(config_text("sk.net"))
     states = g.init_weights(spec, 1)
-    img = g.Rng(55).index_array_u8(512 * 384, 256).reshape(512, 384)
-    proc = g.Processor(spec, states)
+    img = g.Rng(55).index_array_u8(512 * 512, 256).reshape(512, 512)
+    proc = g.Processor(spec, states, retile=0)  # exactly the caller's tiles
     lab128, pr128 = proc.run(img, 128, 101)
+    assert proc.last_tile() == 128
     for w in (200, 256):
         lab, pr = proc.run(img, w, 101)
+        assert proc.last_tile() == w
         assert np.array_equal(lab, lab128)
         assert_bitwise(pr, pr128, f"tile {w}")
+    auto = g.Processor(spec, states)  # internal retiling (default): same planes, fewer FLOPs
+    lab, pr = auto.run(img, 128, 101)
+    assert auto.last_tile() == 512
+    assert np.array_equal(lab, lab128)
+    assert_bitwise(pr, pr128, "retiled")
     n = g.tile_rows(512, 128)
     cuts = [0, 1, 3, n]
+    proc = auto  # bands through the retiling path
     lab = np.zeros_like(lab128)
     pr = np.zeros_like(pr128)
     for r0, r1 in zip(cuts[:-1], cuts[1:]):
