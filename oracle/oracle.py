@@ -91,6 +91,8 @@ _REF_SIGS = {
     "ref_net_blob_shape": (_i, [_vp, C.c_char_p, C.POINTER(_i), C.POINTER(_i), C.POINTER(_i)]),
     "ref_net_blob": (_i, [_vp, C.c_char_p, _vp]),
     "ref_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
+    "ref_save_weights": (_i, [_vp, C.c_char_p]),
+    "ref_write_pgm": (_i, [C.c_char_p, _vp, _i, _i]),
 }
 
 
@@ -420,6 +422,14 @@ class RefNet:
         return labels, probs
 
     n_classes = 2
+
+    def save_weights(self, path: str):
+        _chk(ref().ref_save_weights(self.h, path.encode()), ref().ref_last_error)
+
+
+def write_pgm(path: str, img):
+    img = np.ascontiguousarray(img, np.uint8)
+    _chk(ref().ref_write_pgm(path.encode(), p(img), *img.shape), ref().ref_last_error)
 
 
 def correct_sw(text: str) -> str:

@@ -13,11 +13,13 @@
 #include <vector>
 
 #include "pixelseg/convert.hpp"
+#include "pixelseg/image_io.hpp"
 #include "pixelseg/layers.hpp"
 #include "pixelseg/netgraph.hpp"
 #include "pixelseg/netspec.hpp"
 #include "pixelseg/pipeline.hpp"
 #include "pixelseg/tensor.hpp"
+#include "pixelseg/weights_io.hpp"
 
 using namespace pixelseg;
 
@@ -292,6 +294,25 @@ int ref_process(void* h, const uint8_t* img, int H, int W, int w, int v, uint8_t
     for (std::size_t c = 0; c < r.probs.size(); ++c)
       std::memcpy(probs + c * static_cast<std::size_t>(H) * W, r.probs[c].pix.data(),
                   sizeof(float) * r.probs[c].size());
+  });
+}
+
+
+// ---- file formats (fixtures for the CLI tests) ----
+// save_weights (weights_io.hpp): the net's current parameters as a PXSG file.
+int ref_save_weights(void* h, const char* path) {
+  return guard([&] {
+    RefNet* n = static_cast<RefNet*>(h);
+    save_weights(path, n->spec, n->states);
+  });
+}
+
+// write_pgm (image_io.hpp:83-93).
+int ref_write_pgm(const char* path, const uint8_t* img, int H, int W) {
+  return guard([&] {
+    Plane<std::uint8_t> p(H, W);
+    std::memcpy(p.pix.data(), img, p.size());
+    write_pgm(path, p);
   });
 }
 

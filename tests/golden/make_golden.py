@@ -292,9 +292,70 @@ def configs():
     print("configs.npz", len(f), "arrays")
 
 
+CLI_NET = """input w=229 f=3
+layer conv1 conv_sk k=7 d=1 fout=6 in=data out=conv1 init=gaussian:0.1
+layer relu1 relu in=conv1 out=relu1
+layer pool1 pool_max k=2 s=1 d=1 in=relu1 out=pool1
+layer conv2 conv_sk k=5 d=2 fout=8 in=pool1 out=conv2 init=gaussian:0.1
+layer relu2 relu in=conv2 out=relu2
+layer pool2 pool_max k=2 s=1 d=2 in=relu2 out=pool2
+layer conv3 conv_sk k=3 d=4 fout=12 in=pool2 out=conv3 init=gaussian:0.1
+layer relu3 relu in=conv3 out=relu3
+layer pool3 pool_max k=2 s=1 d=4 in=relu3 out=pool3
+layer ip1 conv_sk k=10 d=8 fout=16 in=pool3 out=ip1 init=gaussian:0.1
+layer relu4 relu in=ip1 out=relu4
+layer ip2 conv_sk k=1 d=1 fout=8 in=relu4 out=ip2 init=gaussian:0.1
+layer relu5 relu in=ip2 out=relu5
+layer ip3 conv_sk k=1 d=1 fout=2 in=relu5 out=ip3 init=gaussian:0.1
+layer prob softmax_loss in=ip3 out=prob
+"""
+
+
+def write_png_gray(path, img):
+    """8-bit grayscale, non-interlaced PNG (filter 0 rows), read by image_io.hpp:95-174."""
+    import struct
+    import zlib
+
+    def chunk(tag, data):
+        return (struct.pack(">I", len(data)) + tag + data +
+                struct.pack(">I", zlib.crc32(tag + data) & 0xFFFFFFFF))
+
+    h, w = img.shape
+    raw = b"".join(b"\x00" + img[y].tobytes() for y in range(h))
+    with open(path, "wb") as fh:
+        fh.write(b"\x89PNG\r\n\x1a\n" + chunk(b"IHDR", struct.pack(">IIBBBBB", w, h, 8, 0, 0, 0, 0))
+                 + chunk(b"IDAT", zlib.compress(raw)) + chunk(b"IEND", b""))
+
+
+def cli():
+    """Fixtures for `pixelseg_gpu process` (proj/tools/pixelseg.cpp:161-191): a reduced-channel
+    sk.net spec file, its PXSG weights written by the reference's save_weights
+    (weights_io.hpp), a 300x260 gray scan written by the reference's write_pgm (and the same
+    pixels as PNG), and the expected output files: labels from the reference's process<float>
+    at the CLI's default tile (128) and the 8-bit probability maps the CLI derives from the
+    probs (clamp to [0,1], lround(p*255), pixelseg.cpp:179-183)."""
+    d = os.path.join(OUT, "cli")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "sk_small.net"), "w") as fh:
+        fh.write(CLI_NET)
+    net = O.RefNet(CLI_NET, seed=3)
+    net.save_weights(os.path.join(d, "sk_small.pxsg"))
+    img = O.Rng(55).index_u8(300 * 260).reshape(300, 260)
+    O.write_pgm(os.path.join(d, "scan.pgm"), img)
+    write_png_gray(os.path.join(d, "scan.png"), img)
+    labels, probs = net.process(img, 128, 101)
+    O.write_pgm(os.path.join(d, "expect_scan_labels.pgm"), labels)
+    for c in range(probs.shape[0]):
+        m = np.floor(np.clip(probs[c].astype(np.float64), 0.0, 1.0) * 255.0 + 0.5).astype(np.uint8)
+        O.write_pgm(os.path.join(d, f"expect_scan_prob{c}.pgm"), m)
+    np.save(os.path.join(d, "expect_scan_probs.npy"), probs)
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["small"]:
-        if arg == "small":
+        if arg == "cli":
+            cli()
+        elif arg == "small":
             configs()
             small()
             nets()
