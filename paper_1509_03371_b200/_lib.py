@@ -35,6 +35,9 @@ OPT_KEEP_BLOBS = 3
 OPT_RETILE = 5
 OPT_LAST_TILE = 6
 
+TC_BF16 = 1
+TC_TF32 = 2
+
 
 class CudaError(Error):
     """A CUDA runtime failure inside libgraft_cuda (no reference counterpart)."""
@@ -120,6 +123,7 @@ _SIGS = {
     "graft_rng_fill_uniform_f32": (_i, [_vp, _vp, _sz, _d, _d]),
     "graft_rng_fill_uniform_f64": (_i, [_vp, _vp, _sz, _d, _d]),
     "graft_rng_fill_index_u8": (_i, [_vp, _vp, _sz, _u64]),
+    "graft_conv_tc_f32": (_i, [_i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),
 }

@@ -44,6 +44,27 @@ void conv_tma(const double* in, const double* w_tiled, const float* bias, const 
 void conv_f64_muladd(const double* in, const double* w, const double* bias, const ConvShape& sh,
                      double* out, cudaStream_t st);
 
+// ---- conv_tc.cu (tolerance mode, opt-in) ---------------------------------------------------
+// tcgen05 implicit-GEMM conv: bf16 (kind::f16) or tf32 (kind::tf32) operands, f32 accumulation
+// in TMEM. NOT bit-exact; see conv_tc.cu and DESIGN.md "Tolerance mode".
+enum { TC_BF16 = 1, TC_TF32 = 2 };
+struct TcShape {
+  int B = 1, C = 0, H = 0, W = 0;  // input, NHWC per image
+  int M = 0, k = 1, d = 1, s = 1, p = 0;
+  int OH = 0, OW = 0;
+  int out_wp = 0;                  // output row pitch (elements; 0 = OW)
+};
+int tc_block_k(int kind);
+size_t tc_elem_bytes(int kind);
+bool conv_tc_eligible(int kind, const TcShape& sh);
+void weights_to_tc(int kind, const float* w, int M, int C, int k, void* out, cudaStream_t st);
+template <typename S>
+void chw_to_nhwc(int kind, const S* in, int B, int C, int H, int W, int wp, void* out, cudaStream_t st);
+// out (f32, or f64 widened f32 when out_f64) = conv + bias (relu'd when relu); out_relu
+// (f64 only, nullable) = relu(conv + bias). CHW per image, row pitch sh.out_wp.
+void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, const TcShape& sh,
+             void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st);
+
 // ---- layers.cu ------------------------------------------------------------------------------
 void f32_to_f64(const float* in, double* out, size_t n, cudaStream_t st);
 void f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);

@@ -102,7 +102,7 @@ def test_cli_process_matches_reference_files(tmp_path, image):
 
 @pytest.mark.gpu
 @needs_bin
-@pytest.mark.parametrize("tile", [64, 37, 300])
+@pytest.mark.parametrize("tile", [64, 37, 260])
 def test_cli_process_any_tile_same_labels(tmp_path, tile):
     """The labelling does not depend on the tile (pipeline.hpp:662-672; test_pipeline.cpp:535-588)."""
     out = tmp_path / "out"

@@ -1,0 +1,77 @@
+"""Tolerance mode: the tcgen05 implicit-GEMM conv (csrc/conv_tc.cu) against
+an fp64 torch conv of the same rounded operands.
+
+The tensor-core path is NOT the reference's arithmetic (inc/tensor.hpp:151-169: an fp64 chain
+rounded once to f32): operands are rounded to bf16 / tf32 and products are summed in f32 by the
+tensor core. Stated tolerance: against the exact sum of the rounded
+operands, |got - ref| <= 4e-5 * sum_k |w_k x_k| + 1 ulp(f32) per output."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import paper_1509_03371_b200 as g  # noqa: E402
+from paper_1509_03371_b200 import _lib  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+TOL = 4e-5
+
+
+def round_tf32(t):
+    """cvt.rna.tf32.f32: round to 10 mantissa bits, ties away from zero."""
+    b = t.contiguous().view(torch.int32)
+    b = (b + 0x1000) & ~0x1FFF
+    return b.view(torch.float32)
+
+
+def run_tc(kind, x, w, bias, k, d, relu):
+    B, C, H, W = x.shape
+    M = w.shape[0]
+    OH, OW = H - (k - 1) * d, W - (k - 1) * d
+    out = torch.empty(B, M, OH, OW, device="cuda", dtype=torch.float32)
+    torch.cuda.synchronize()
+    _lib.check(_lib.lib().graft_conv_tc_f32(kind, x.data_ptr(), B, C, H, W, w.data_ptr(),
+                                            bias.data_ptr(), M, k, d, out.data_ptr(), int(relu)))
+    return out
+
+
+CASES = [  # B, C, H, W, M, k, d
+    (1, 64, 20, 20, 128, 3, 1),
+    (2, 64, 30, 300, 128, 3, 2),    # ragged row segments (OW = 296 > 256)
+    (1, 128, 36, 40, 256, 3, 4),    # conv3-like dilation
+    (1, 192, 90, 90, 128, 10, 8),   # ip1 geometry (k10 d8), 18x18 out
+    (1, 1024, 8, 130, 512, 1, 1),   # ip2 geometry (1x1, K = 1024)
+]
+
+
+@pytest.mark.parametrize("kind", [_lib.TC_BF16, _lib.TC_TF32])
+@pytest.mark.parametrize("case", CASES)
+def test_conv_tc_matches_fp64_conv_of_rounded_operands(kind, case):
+    B, C, H, W, M, k, d = case
+    gen = torch.Generator(device="cuda").manual_seed(1234 + C + k)
+    x = torch.rand(B, C, H, W, device="cuda", generator=gen) * 2 - 1
+    w = (torch.randn(M, C, k, k, device="cuda", generator=gen) * (2.0 / (C * k * k)) ** 0.5)
+    bias = torch.randn(M, device="cuda", generator=gen) * 0.01
+    for relu in (False, True):
+        got = run_tc(kind, x, w, bias, k, d, relu)
+        if kind == _lib.TC_BF16:
+            xr, wr = x.bfloat16().double(), w.bfloat16().double()
+        else:
+            xr, wr = round_tf32(x).double(), round_tf32(w).double()
+        ref = torch.nn.functional.conv2d(xr, wr, bias.double(), dilation=d)
+        if relu:
+            ref = ref.clamp_min(0)
+        absum = torch.nn.functional.conv2d(xr.abs(), wr.abs(), None, dilation=d)
+        err = (got.double() - ref).abs()
+        bound = TOL * absum + ref.abs() * 2.0 ** -23 + 1e-30
+        worst = (err / bound).max().item()
+        assert worst <= 1.0, f"kind {kind} case {case} relu {relu}: err/bound {worst:.3g}"
+
+
+def test_conv_tc_rejects_ineligible_shapes():
+    x = torch.zeros(1, 48, 10, 10, device="cuda")
+    w = torch.zeros(128, 48, 3, 3, device="cuda")
+    b = torch.zeros(128, device="cuda")
+    with pytest.raises(ValueError, match="channels"):
+        run_tc(_lib.TC_BF16, x, w, b, 3, 1, False)
