@@ -34,6 +34,7 @@ OPT_TILE_BATCH = 2
 OPT_KEEP_BLOBS = 3
 OPT_RETILE = 5
 OPT_LAST_TILE = 6
+OPT_TC_KIND = 7
 
 TC_BF16 = 1
 TC_TF32 = 2

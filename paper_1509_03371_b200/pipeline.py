@@ -67,9 +67,13 @@ class Processor:
     """A device-resident net for repeated process() calls (one upload of the weights)."""
 
     def __init__(self, spec: NetSpec, states: NetStates, tile_batch: int = 0,
-                 retile: Optional[int] = None):
+                 retile: Optional[int] = None, tensor_cores: Optional[str] = None):
         """retile: largest internal tile process() may use (default 1024; 0 = exactly the
-        caller's w). Every tiling gives bit-identical planes."""
+        caller's w). Every tiling gives bit-identical planes.
+
+        tensor_cores: None (default) = the exact fp64 path, bit-identical to the reference;
+        "bf16" / "tf32" = TOLERANCE MODE: eligible convs run on the tcgen05 tensor cores and the
+        planes are only within the tolerance DESIGN.md states (labels may differ on near-ties)."""
         self.spec = spec
         self.states = states
         self.net = DeviceNet(spec)
@@ -78,6 +82,11 @@ class Processor:
             self.net.set_option(_lib.OPT_TILE_BATCH, tile_batch)
         if retile is not None:
             self.net.set_option(_lib.OPT_RETILE, retile)
+        if tensor_cores is not None:
+            kinds = {"bf16": _lib.TC_BF16, "tf32": _lib.TC_TF32}
+            if tensor_cores not in kinds:
+                raise ValueError(f"tensor_cores must be None, 'bf16' or 'tf32', not {tensor_cores!r}")
+            self.net.set_option(_lib.OPT_TC_KIND, kinds[tensor_cores])
         self.n_classes = compute_channels(spec)[spec.layers[-1].output]
 
     def run(self, image: np.ndarray, w: int, v: int, labels: Optional[np.ndarray] = None,

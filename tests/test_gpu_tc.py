@@ -75,3 +75,33 @@ def test_conv_tc_rejects_ineligible_shapes():
     b = torch.zeros(128, device="cuda")
     with pytest.raises(ValueError, match="channels"):
         run_tc(_lib.TC_BF16, x, w, b, 3, 1, False)
+
+
+def test_process_tolerance_mode_full_sk_net():
+    """process() of full sk.net with ip1/ip2 on the tensor cores (bf16) vs the exact mode on the
+    same 256x256 image: the exact planes are the reference's (tests/test_gpu_net.py); the
+    tolerance-mode planes must stay within the stated tolerance and the labels may only differ
+    where the exact probabilities are within that tolerance of a tie."""
+    from conftest import config_text
+
+    spec = g.parse_netspec_or_throw(config_text("sk"))
+    states = g.init_weights(spec, 1)
+    img = g.Rng(55).index_array_u8(256 * 256, 256).reshape(256, 256)
+    lab_x, prob_x = g.Processor(spec, states).run(img, 128, 101)
+    for kind in ("bf16", "tf32"):
+        proc = g.Processor(spec, states, tensor_cores=kind)
+        lab_t, prob_t = proc.run(img, 128, 101)
+        dp = np.abs(prob_t - prob_x)
+        assert dp.max() <= 1e-4, f"{kind}: max |dprob| {dp.max():.3g}"
+        margin = np.abs(prob_x[1] - prob_x[0])
+        bad = lab_t != lab_x
+        assert np.all(margin[bad] <= 2e-4), f"{kind}: a label flipped away from a near-tie"
+        assert bad.mean() <= 1e-3
+
+
+def test_tolerance_mode_option_validation():
+    from conftest import config_text
+
+    spec = g.parse_netspec_or_throw(config_text("sk"))
+    with pytest.raises(ValueError):
+        g.Processor(spec, g.init_weights(spec, 1), tensor_cores="fp8")
