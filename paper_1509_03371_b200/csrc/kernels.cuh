@@ -56,6 +56,12 @@ struct TcShape {
 };
 int tc_block_k(int kind);
 size_t tc_elem_bytes(int kind);
+// Operand layouts pad channels to the 128-byte K block and f_out to the 128-row MMA tile
+// with zeros: [Mp][k][k][Cp] weights, [B][H][W][Cp] activations.
+int tc_padded_c(int kind, int C);
+int tc_padded_m(int M);
+size_t tc_weight_bytes(int kind, int M, int C, int k);
+size_t tc_input_bytes(int kind, int B, int C, int H, int W);
 bool conv_tc_eligible(int kind, const TcShape& sh);
 void weights_to_tc(int kind, const float* w, int M, int C, int k, void* out, cudaStream_t st);
 template <typename S>

@@ -224,13 +224,12 @@ int run_layers(graft_net& n, bool mode_process) {
           ts.out_wp = sh.out_wp;
           if (n.tc_kind && conv_tc_eligible(n.tc_kind, ts)) {
             // tolerance mode: tcgen05 tensor cores, bf16/tf32 operands (not bit-exact)
-            const size_t es = tc_elem_bytes(n.tc_kind);
             if (l.w_tc_kind != n.tc_kind) {
-              l.w_tc.ensure(static_cast<size_t>(l.f_out) * fan_in * es);
+              l.w_tc.ensure(tc_weight_bytes(n.tc_kind, l.f_out, in.C, l.k));
               weights_to_tc(n.tc_kind, l.w_f32.as<float>(), l.f_out, in.C, l.k, l.w_tc.p, n.stream);
               l.w_tc_kind = n.tc_kind;
             }
-            n.tc_in.ensure(static_cast<size_t>(B) * in.C * in.H * in.W * es);
+            n.tc_in.ensure(tc_input_bytes(n.tc_kind, B, in.C, in.H, in.W));
             chw_to_nhwc<double>(n.tc_kind, in.buf.as<double>(), B, in.C, in.H, in.W, in.Wp,
                                 n.tc_in.p, n.stream);
             conv_tc(n.tc_kind, n.tc_in.p, l.w_tc.p, l.bias_dev.as<float>(), ts, out, out_relu,

@@ -42,6 +42,9 @@ CASES = [  # B, C, H, W, M, k, d
     (1, 128, 36, 40, 256, 3, 4),    # conv3-like dilation
     (1, 192, 90, 90, 128, 10, 8),   # ip1 geometry (k10 d8), 18x18 out
     (1, 1024, 8, 130, 512, 1, 1),   # ip2 geometry (1x1, K = 1024)
+    (1, 48, 30, 40, 128, 5, 2),     # conv2: channels padded 48 -> 64 (bf16) / 64 (tf32)
+    (1, 128, 40, 40, 192, 3, 4),    # conv3: f_out padded 192 -> 256
+    (2, 3, 30, 30, 48, 7, 1),       # conv1: 3 channels, 48 outputs
 ]
 
 
@@ -69,12 +72,13 @@ def test_conv_tc_matches_fp64_conv_of_rounded_operands(kind, case):
         assert worst <= 1.0, f"kind {kind} case {case} relu {relu}: err/bound {worst:.3g}"
 
 
-def test_conv_tc_rejects_ineligible_shapes():
-    x = torch.zeros(1, 48, 10, 10, device="cuda")
-    w = torch.zeros(128, 48, 3, 3, device="cuda")
+def test_conv_tc_rejects_empty_geometry():
+    x = torch.zeros(1, 48, 4, 4, device="cuda")
+    w = torch.zeros(128, 48, 5, 5, device="cuda")
     b = torch.zeros(128, device="cuda")
-    with pytest.raises(ValueError, match="channels"):
-        run_tc(_lib.TC_BF16, x, w, b, 3, 1, False)
+    with pytest.raises(g.SizeError):
+        _lib.check(_lib.lib().graft_conv_tc_f32(_lib.TC_BF16, x.data_ptr(), 1, 48, 4, 4, w.data_ptr(),
+                                                b.data_ptr(), 128, 5, 1, x.data_ptr(), 0))
 
 
 def test_process_tolerance_mode_full_sk_net():
