@@ -92,6 +92,13 @@ _REF_SIGS = {
     "ref_net_blob": (_i, [_vp, C.c_char_p, _vp]),
     "ref_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp]),
     "ref_save_weights": (_i, [_vp, C.c_char_p]),
+    "ref_net_zero_blob_diffs": (_i, [_vp]),
+    "ref_net_set_blob_diff": (_i, [_vp, C.c_char_p, _vp]),
+    "ref_net_blob_diff": (_i, [_vp, C.c_char_p, _vp]),
+    "ref_net_backward": (_i, [_vp]),
+    "ref_net_param_state": (None, [_vp, _i, _i, _vp, _vp]),
+    "ref_net_softmax_loss": (_i, [_vp, C.c_char_p, _vp, _vp, _i, _i, C.POINTER(_d)]),
+    "ref_net_sgd_step": (_i, [_vp, _d, _d, _d]),
     "ref_write_pgm": (_i, [C.c_char_p, _vp, _i, _i]),
 }
 
@@ -422,6 +429,42 @@ class RefNet:
         return labels, probs
 
     n_classes = 2
+
+    # ---- training step (the reference's NetRunner::backward, softmax_loss, sgd_step) ----
+    def zero_blob_diffs(self):
+        _chk(ref().ref_net_zero_blob_diffs(self.h), ref().ref_last_error)
+
+    def set_blob_diff(self, name: str, diff):
+        d = np.ascontiguousarray(diff, np.float32)
+        _chk(ref().ref_net_set_blob_diff(self.h, name.encode(), p(d)), ref().ref_last_error)
+
+    def blob_diff(self, name: str) -> np.ndarray:
+        shape = self.blob(name).shape
+        out = np.empty(shape, np.float32)
+        _chk(ref().ref_net_blob_diff(self.h, name.encode(), p(out)), ref().ref_last_error)
+        return out
+
+    def backward(self):
+        _chk(ref().ref_net_backward(self.h), ref().ref_last_error)
+
+    def param_state(self, layer: int, which: int):
+        nw, nb = C.c_longlong(), C.c_longlong()
+        ref().ref_net_param_sizes(self.h, layer, C.byref(nw), C.byref(nb))
+        w = np.empty(nw.value, np.float32)
+        b = np.empty(nb.value, np.float32)
+        ref().ref_net_param_state(self.h, layer, which, p(w), p(b))
+        return w, b
+
+    def softmax_loss(self, scores: str, labels, mask=None) -> float:
+        lab = np.ascontiguousarray(labels, np.int32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        loss = C.c_double()
+        _chk(ref().ref_net_softmax_loss(self.h, scores.encode(), p(lab), p(m), lab.shape[0],
+                                        lab.shape[1], C.byref(loss)), ref().ref_last_error)
+        return loss.value
+
+    def sgd_step(self, lr: float, momentum: float, weight_decay: float):
+        _chk(ref().ref_net_sgd_step(self.h, lr, momentum, weight_decay), ref().ref_last_error)
 
     def save_weights(self, path: str):
         _chk(ref().ref_save_weights(self.h, path.encode()), ref().ref_last_error)

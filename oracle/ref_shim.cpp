@@ -316,4 +316,72 @@ int ref_write_pgm(const char* path, const uint8_t* img, int H, int W) {
   });
 }
 
+// ---- training step ----
+static NetRunner<float>& runner_of(RefNet* n) {
+  if (!n->runner) throw SpecError("no runner (run forward first)");
+  return *n->runner;
+}
+
+int ref_net_zero_blob_diffs(void* h) {
+  return guard([&] { runner_of(static_cast<RefNet*>(h)).zero_blob_diffs(); });
+}
+
+// blob_mut(name).diff = src (the caller's seeding, netgraph.hpp:85-87)
+int ref_net_set_blob_diff(void* h, const char* name, const float* src) {
+  return guard([&] {
+    Blob<float>& b = runner_of(static_cast<RefNet*>(h)).blob_mut(name);
+    b.diff.assign(src, src + b.size());
+  });
+}
+
+// Blob::diff of a blob (zeros when the diff is empty).
+int ref_net_blob_diff(void* h, const char* name, float* dst) {
+  return guard([&] {
+    const Blob<float>& b = runner_of(static_cast<RefNet*>(h)).blob(name);
+    if (b.diff.size() == b.size())
+      std::memcpy(dst, b.diff.data(), sizeof(float) * b.size());
+    else
+      std::memset(dst, 0, sizeof(float) * b.size());
+  });
+}
+
+int ref_net_backward(void* h) {
+  return guard([&] { runner_of(static_cast<RefNet*>(h)).backward(); });
+}
+
+// which: 1 = weight_diff/bias_diff, 2 = weight_mom/bias_mom
+void ref_net_param_state(void* h, int layer, int which, float* w, float* b) {
+  const LayerState<float>& st = static_cast<RefNet*>(h)->states.layers[layer];
+  const auto& vw = which == 1 ? st.weight_diff : st.weight_mom;
+  const auto& vb = which == 1 ? st.bias_diff : st.bias_mom;
+  if (w) std::memcpy(w, vw.data(), sizeof(float) * vw.size());
+  if (b) std::memcpy(b, vb.data(), sizeof(float) * vb.size());
+}
+
+// softmax_loss (layers.hpp:269-307) on the runner's blob; mask may be NULL.
+int ref_net_softmax_loss(void* h, const char* scores, const int* labels, const uint8_t* mask,
+                         int H, int W, double* loss) {
+  return guard([&] {
+    Blob<float>& s = runner_of(static_cast<RefNet*>(h)).blob_mut(scores);
+    Plane<int> lab(H, W);
+    std::memcpy(lab.pix.data(), labels, sizeof(int) * lab.size());
+    Plane<std::uint8_t> m;
+    if (mask) {
+      m = Plane<std::uint8_t>(H, W);
+      std::memcpy(m.pix.data(), mask, m.size());
+    }
+    *loss = softmax_loss(s, lab, m);
+  });
+}
+
+int ref_net_sgd_step(void* h, double lr, double momentum, double weight_decay) {
+  return guard([&] {
+    SolverConfig cfg;
+    cfg.lr = lr;
+    cfg.momentum = momentum;
+    cfg.weight_decay = weight_decay;
+    sgd_step(static_cast<RefNet*>(h)->states, cfg);
+  });
+}
+
 }  // extern "C"

@@ -12,7 +12,7 @@ from .netspec import (InitKind, LayerKind, LayerSpec, NetSpec, compute_channels,
                       propagate_sizes)
 from .layers import (conv_sk_forward, gemm, gemm_flops, im2col_sk, maxpool_sk_forward,
                      mergecrop_forward, relu_forward, softmax_forward, upconv_forward)
-from .netgraph import NetRunner, NetStates, init_weights
+from .netgraph import NetRunner, NetStates, SolverConfig, init_weights, sgd_step
 from .pipeline import (ProcessResult, Processor, band_rows, mirror_pad, normalize_image, process,
                        tile_rows)
 from .rng import Rng
@@ -23,6 +23,6 @@ __all__ = [
     "compute_channels", "flop_estimate", "load_netspec", "output_extent", "parse_netspec",
     "parse_netspec_or_throw", "propagate_sizes", "conv_sk_forward", "gemm", "gemm_flops",
     "im2col_sk", "maxpool_sk_forward", "mergecrop_forward", "relu_forward", "softmax_forward",
-    "upconv_forward", "NetRunner", "NetStates", "init_weights", "ProcessResult", "Processor",
+    "upconv_forward", "NetRunner", "NetStates", "SolverConfig", "init_weights", "sgd_step", "ProcessResult", "Processor",
     "band_rows", "mirror_pad", "normalize_image", "process", "tile_rows", "Rng",
 ]

@@ -35,6 +35,9 @@ OPT_KEEP_BLOBS = 3
 OPT_RETILE = 5
 OPT_LAST_TILE = 6
 OPT_TC_KIND = 7
+OPT_TRAINING = 8
+PARAM_DIFF = 1
+PARAM_MOMENTUM = 2
 
 TC_BF16 = 1
 TC_TF32 = 2
@@ -125,6 +128,14 @@ _SIGS = {
     "graft_rng_fill_uniform_f64": (_i, [_vp, _vp, _sz, _d, _d]),
     "graft_rng_fill_index_u8": (_i, [_vp, _vp, _sz, _u64]),
     "graft_conv_tc_f32": (_i, [_i, _vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i]),
+    "graft_net_zero_blob_diffs": (_i, [_vp]),
+    "graft_net_set_blob_diff_f32": (_i, [_vp, C.c_char_p, _vp, _i]),
+    "graft_net_blob_diff_f32": (_i, [_vp, C.c_char_p, _vp, _i]),
+    "graft_net_backward": (_i, [_vp]),
+    "graft_net_get_param_state_f32": (_i, [_vp, _i, _i, _vp, _vp]),
+    "graft_net_set_param_state_f32": (_i, [_vp, _i, _i, _vp, _vp]),
+    "graft_net_softmax_loss_f32": (_i, [_vp, C.c_char_p, _vp, _vp, _i, _i, C.POINTER(_d)]),
+    "graft_net_sgd_step": (_i, [_vp, _d, _d, _d]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),
 }

@@ -71,6 +71,35 @@ void chw_to_nhwc(int kind, const S* in, int B, int C, int H, int W, int wp, void
 void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, const TcShape& sh,
              void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st);
 
+// ---- train.cu: the backward layer functions and sgd_step (bit-identical, S = float) --------
+// Data blobs: widened-f32 f64, row pitch wp; diffs: compact f32 [C][H][W] of one image.
+// gemm (tensor.hpp:151-169) on DMMA: C(i,j) = float(alpha*chain + beta*C), strided A and B.
+void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long long sak,
+                      const double* b, long long sbk, long long sbj, double alpha, double beta,
+                      float* c, cudaStream_t st);
+void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long long sak,
+                      const float* b, long long sbk, long long sbj, double alpha, double beta,
+                      float* c, cudaStream_t st);
+void im2col_pitched(const double* in, int C, int H, int W, int wp, int k, int d, int s, int p,
+                    int OH, int OW, double* col, cudaStream_t st);
+void bias_grad(const float* dout, int M, int n, float* bdiff, cudaStream_t st);
+void col2im_add(const float* colg, int C, int H, int W, int k, int d, int s, int p, int OH, int OW,
+                float* diff, cudaStream_t st);
+void maxpool_backward(const uint64_t* argmax, const float* dout, int C, int H, int W, int k, int d,
+                      int s, int OH, int OW, float* din, cudaStream_t st);
+void relu_backward(const double* data, int rows, int W, int wp, const float* dout, float* din,
+                   cudaStream_t st);
+void upconv_backward(const float* dout, int C, int H, int W, float* din, cudaStream_t st);
+void mergecrop_backward(const float* dout, long long n, float* da, cudaStream_t st);
+void softmax_backward(const double* prob, int C, int H, int W, int wp, const float* dout, float* din,
+                      cudaStream_t st);
+void sgd(float* w, float* mom, float* diff, long long n, float lr, float mu, float wd, cudaStream_t st);
+// softmax_loss (layers.hpp:269-307) over a [C][H][W] score blob (pitched): diff += gradient,
+// *loss (device) = the reference's loss; terms = H*W f64 scratch; n_count = unmasked pixels.
+void softmax_loss(const double* scores, int C, int H, int W, int wp, const int* labels,
+                  const uint8_t* mask, long long n_count, float* diff, double* terms, double* loss,
+                  cudaStream_t st);
+
 // ---- layers.cu ------------------------------------------------------------------------------
 void f32_to_f64(const float* in, double* out, size_t n, cudaStream_t st);
 void f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);

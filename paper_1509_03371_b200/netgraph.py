@@ -131,6 +131,8 @@ class NetRunner:
         self.spec = spec
         self.states = states
         self.net = DeviceNet(spec)
+        # the reference's forward always records what backward needs (pool argmax)
+        self.net.set_option(_lib.OPT_TRAINING, 1)
         self._layer_seconds: List[float] = [0.0] * len(spec.layers)
         self._last = None
 
@@ -173,3 +175,91 @@ class NetRunner:
 
     def layer_seconds(self) -> List[float]:
         return list(self._layer_seconds)
+
+    # ---- training step: backward, softmax_loss, sgd_step ------------
+    def zero_blob_diffs(self) -> None:
+        """NetRunner::zero_blob_diffs (netgraph.hpp:100-105)."""
+        _lib.check(_lib.lib().graft_net_zero_blob_diffs(self.net.h))
+
+    def blob_diff(self, name: str) -> np.ndarray:
+        """Blob::diff of a blob as a (C, H, W) float32 array (zeros when cleared)."""
+        b = self.blob(name)
+        out = np.zeros((b.channels, b.height, b.width), np.float32)
+        if out.size:
+            _lib.check(_lib.lib().graft_net_blob_diff_f32(self.net.h, name.encode(), _lib.ptr(out),
+                                                          _lib.MEM_HOST))
+        return out
+
+    def set_blob_diff(self, name: str, diff: np.ndarray) -> None:
+        """blob_mut(name).diff = diff: the caller's seeding before backward (netgraph.hpp:85-87)."""
+        d = np.ascontiguousarray(diff, np.float32)
+        _lib.check(_lib.lib().graft_net_set_blob_diff_f32(self.net.h, name.encode(), _lib.ptr(d),
+                                                          _lib.MEM_HOST))
+
+    def _push_param_state(self) -> None:
+        for i, l in enumerate(self.spec.layers):
+            if l.kind != LayerKind.ConvSK:
+                continue
+            st = self.states.layers[i]
+            for which, (w, b) in ((_lib.PARAM_DIFF, (st.weight_diff, st.bias_diff)),
+                                  (_lib.PARAM_MOMENTUM, (st.weight_mom, st.bias_mom))):
+                w = np.ascontiguousarray(w, np.float32)
+                b = np.ascontiguousarray(b, np.float32)
+                if w.size == st.weights.size and b.size == st.bias.size:
+                    _lib.check(_lib.lib().graft_net_set_param_state_f32(
+                        self.net.h, i, which, _lib.ptr(w), _lib.ptr(b)))
+
+    def _pull_param_state(self, weights: bool) -> None:
+        for i, l in enumerate(self.spec.layers):
+            if l.kind != LayerKind.ConvSK:
+                continue
+            st = self.states.layers[i]
+            for which, names in ((_lib.PARAM_DIFF, ("weight_diff", "bias_diff")),
+                                 (_lib.PARAM_MOMENTUM, ("weight_mom", "bias_mom"))):
+                w = np.empty(st.weights.size, np.float32)
+                b = np.empty(st.bias.size, np.float32)
+                _lib.check(_lib.lib().graft_net_get_param_state_f32(self.net.h, i, which,
+                                                                    _lib.ptr(w), _lib.ptr(b)))
+                setattr(st, names[0], w)
+                setattr(st, names[1], b)
+            if weights:
+                w = np.empty(st.weights.size, np.float32)
+                b = np.empty(st.bias.size, np.float32)
+                _lib.check(_lib.lib().graft_net_get_params_f32(self.net.h, i, _lib.ptr(w),
+                                                               _lib.ptr(b)))
+                st.weights, st.bias = w, b
+                self.net._uploaded[i] = (w.copy(), b.copy())
+
+    def backward(self) -> None:
+        """NetRunner::backward (netgraph.hpp:88-98) on the device: reverse sweep over the blob
+        diffs seeded since the last forward; parameter diffs accumulate into the NetStates."""
+        self._push_param_state()
+        _lib.check(_lib.lib().graft_net_backward(self.net.h))
+        self._pull_param_state(weights=False)
+
+    def softmax_loss(self, scores: str, labels: np.ndarray, mask=None) -> float:
+        """softmax_loss (layers.hpp:269-307) on this runner's blob `scores` (diff += gradient)."""
+        lab = np.ascontiguousarray(labels, np.int32)
+        m = None if mask is None else np.ascontiguousarray(mask, np.uint8)
+        loss = C.c_double()
+        _lib.check(_lib.lib().graft_net_softmax_loss_f32(self.net.h, scores.encode(), _lib.ptr(lab),
+                                                         _lib.ptr(m), lab.shape[0], lab.shape[1],
+                                                         C.byref(loss)))
+        return loss.value
+
+
+class SolverConfig:
+    """The SGD fields of SolverConfig (pipeline.hpp:324-339) that sgd_step reads."""
+
+    def __init__(self, lr: float = 0.01, momentum: float = 0.9, weight_decay: float = 0.0):
+        self.lr = lr
+        self.momentum = momentum
+        self.weight_decay = weight_decay
+
+
+def sgd_step(runner: NetRunner, cfg: SolverConfig) -> None:
+    """sgd_step<float> (pipeline.hpp:483-500) on the device copy of runner.states:
+    v = mom*v - lr*(diff + wd*w); w += v; diffs zeroed. The NetStates arrays are updated."""
+    runner._push_param_state()
+    _lib.check(_lib.lib().graft_net_sgd_step(runner.net.h, cfg.lr, cfg.momentum, cfg.weight_decay))
+    runner._pull_param_state(weights=True)
