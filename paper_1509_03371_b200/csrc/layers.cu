@@ -463,7 +463,15 @@ __global__ void softmax_loss_kernel(const double* __restrict__ scores, int C, in
 __global__ void loss_sum_kernel(const double* __restrict__ terms, long long n, double inv_n,
                                 double* __restrict__ loss) {
   double acc = 0.0;
-  for (long long i = 0; i < n; ++i) acc = __dadd_rn(acc, -terms[i]);
+  long long i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double t[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) t[u] = terms[i + u];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, -t[u]);
+  }
+  for (; i < n; ++i) acc = __dadd_rn(acc, -terms[i]);
   *loss = __dmul_rn(acc, inv_n);
 }
 

@@ -1,0 +1,99 @@
+"""One SGD training step of sk.net on the B200: forward of one patch,
+softmax_loss, NetRunner::backward, sgd_step -- the loop body of train() (pipeline.hpp:567-600)
+without sampling/augmentation -- bit-identical to the reference. Prints one JSON line.
+
+    python tools/train_bench.py [--w0 229] [--steps 5] [--cpu]   (--cpu: also the reference at w0)
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import paper_1509_03371_b200 as g  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--w0", type=int, default=229)
+ap.add_argument("--steps", type=int, default=5)
+ap.add_argument("--cpu", action="store_true")
+a = ap.parse_args()
+f = np.load(os.path.join(ROOT, "tests", "golden", "configs.npz"))
+text = bytes(f["sk"]).decode()
+spec = g.parse_netspec_or_throw(text)
+states = g.init_weights(spec, 1)
+runner = g.NetRunner(spec, states)
+rng = g.Rng(7)
+x = rng.uniform_array(3 * a.w0 * a.w0, -1.0, 1.0).reshape(3, a.w0, a.w0).astype(np.float32)
+w_out = g.output_extent(spec, a.w0)
+labels = (rng.index_array_u8(w_out * w_out, 2).astype(np.int32)).reshape(w_out, w_out)
+cfg = g.SolverConfig(lr=0.01, momentum=0.9, weight_decay=5e-4)
+scores = spec.layers[-1].inputs[0]
+
+
+def step():
+    runner.forward(g.Blob.from_array(x))
+    runner.zero_blob_diffs()
+    loss = runner.softmax_loss(scores, labels)
+    runner.backward()
+    g.sgd_step(runner, cfg)
+    return loss
+
+
+step()
+ts = []
+for _ in range(a.steps):
+    t = time.perf_counter()
+    loss = step()
+    ts.append(time.perf_counter() - t)
+
+# the same step straight through the C ABI (device-resident state, no NetStates sync)
+from paper_1509_03371_b200 import _lib  # noqa: E402
+import ctypes as C  # noqa: E402
+
+L = _lib.lib()
+h = runner.net.h
+xs = np.ascontiguousarray(x)
+phases = {"forward": 0.0, "softmax_loss": 0.0, "backward": 0.0, "sgd_step": 0.0}
+lossv = C.c_double()
+oc, oh, ow = C.c_int(), C.c_int(), C.c_int()
+for it in range(a.steps + 1):
+    t0 = time.perf_counter()
+    _lib.check(L.graft_net_forward_f32(h, _lib.ptr(xs), 3, a.w0, a.w0, _lib.MEM_HOST, C.byref(oc),
+                                       C.byref(oh), C.byref(ow)))
+    t1 = time.perf_counter()
+    _lib.check(L.graft_net_zero_blob_diffs(h))
+    _lib.check(L.graft_net_softmax_loss_f32(h, scores.encode(), _lib.ptr(labels), None, w_out, w_out,
+                                            C.byref(lossv)))
+    t2 = time.perf_counter()
+    _lib.check(L.graft_net_backward(h))
+    t3 = time.perf_counter()
+    _lib.check(L.graft_net_sgd_step(h, cfg.lr, cfg.momentum, cfg.weight_decay))
+    t4 = time.perf_counter()
+    if it:
+        for k, v in zip(phases, (t1 - t0, t2 - t1, t3 - t2, t4 - t3)):
+            phases[k] += v / a.steps
+fwd = g.flop_estimate(spec, a.w0)["total"]
+line = {"what": "sk.net training step (forward + softmax_loss + backward + sgd_step), one patch",
+        "w0": a.w0, "labels_per_step": w_out * w_out, "ms_per_step": 1e3 * min(ts),
+        "forward_flop": fwd, "step_flop_approx": 3 * fwd,
+        "tflops_approx": 3 * fwd / min(ts) / 1e12, "loss": loss,
+        "c_abi_ms_per_phase": {k: 1e3 * v for k, v in phases.items()},
+        "c_abi_ms_per_step": 1e3 * sum(phases.values()),
+        "note": "host wall clock around the synchronous C-ABI calls; includes the Python mirror's "
+                "NetStates sync (parameter diffs/momenta/weights D2H each step)"}
+if a.cpu:
+    from oracle import oracle as O
+    ref = O.RefNet(text, seed=1)
+    t = time.perf_counter()
+    ref.forward(x)
+    ref.zero_blob_diffs()
+    ref.softmax_loss(scores, labels)
+    ref.backward()
+    ref.sgd_step(cfg.lr, cfg.momentum, cfg.weight_decay)
+    line["reference_cpu_ms_per_step"] = 1e3 * (time.perf_counter() - t)
+    line["reference_cpu_threads"] = 1
+print(json.dumps(line), flush=True)
