@@ -171,7 +171,85 @@ static void process_cases() {
   CHECK(!e1.empty() && e1 == e2, "process tile error");
 }
 
+// Training step: reference NetRunner::backward / softmax_loss / sgd_step
+// vs the drop-ins, two SGD iterations, plus a diff seeded through blob_mut (test_netgraph.cpp).
+static void train_cases() {
+  const char* texts[] = {
+      "input w=12 f=2\n"
+      "layer conv1 conv_sk k=3 fout=4 in=data out=conv1 init=gaussian:0.5\n"
+      "layer relu1 relu in=conv1 out=relu1\n"
+      "layer pool1 pool_max k=2 s=2 in=relu1 out=pool1\n"
+      "layer conv2 conv_sk k=3 fout=3 in=pool1 out=conv2 init=gaussian:0.5\n"
+      "layer prob softmax_loss in=conv2 out=prob\n",
+      "input w=16 f=1\n"
+      "layer conv1 conv_sk k=3 fout=2 in=data out=conv1 init=gaussian:0.4\n"
+      "layer pool1 pool_max k=2 s=2 in=conv1 out=pool1\n"
+      "layer conv2 conv_sk k=3 fout=4 in=pool1 out=conv2 init=gaussian:0.4\n"
+      "layer up1 upconv in=conv2 out=up1\n"
+      "layer merge1 mergecrop in=up1,conv1 out=merge1\n"
+      "layer conv3 conv_sk k=3 d=2 fout=2 in=merge1 out=conv3 init=gaussian:0.4\n"
+      "layer prob softmax_loss in=conv3 out=prob\n"};
+  for (const char* text : texts) {
+    const NetSpec spec = parse_netspec_or_throw(text);
+    NetStates<float> s_ref = init_weights<float>(spec, 7), s_gpu = init_weights<float>(spec, 7);
+    NetRunner<float> ref(spec, s_ref);
+    gpu::NetRunner<float> got(spec, s_gpu);
+    SolverConfig cfg;
+    cfg.lr = 0.05;
+    cfg.momentum = 0.9;
+    cfg.weight_decay = 5e-4;
+    Rng rng(3);
+    const std::string scores = spec.layers.back().inputs[0];
+    for (int it = 0; it < 2; ++it) {
+      Blob<float> x(spec.f0, spec.w0, spec.w0);
+      fill(x.data, rng);
+      const Blob<float>& o1 = ref.forward(x);
+      const Blob<float>& o2 = got.forward(x);
+      CHECK(same_bits(o1.data, o2.data), "train forward");
+      ref.zero_blob_diffs();
+      got.zero_blob_diffs();
+      Plane<int> lab(o1.height, o1.width);
+      for (auto& v : lab.pix) v = static_cast<int>(rng.uniform_index(o1.channels));
+      Plane<std::uint8_t> mask(o1.height, o1.width, 1);
+      for (auto& v : mask.pix) v = rng.coin() ? 1 : 0;
+      const double l1 = softmax_loss(ref.blob_mut(scores), lab, mask);
+      const double l2 = gpu::softmax_loss(got, scores, lab, mask);
+      CHECK(std::memcmp(&l1, &l2, sizeof l1) == 0, "softmax_loss");
+      ref.backward();
+      got.backward();
+      for (const auto& l : spec.layers)
+        CHECK(same_bits(ref.blob(l.output).diff, got.blob_mut(l.output).diff), "backward blob diff");
+      for (std::size_t i = 0; i < spec.layers.size(); ++i) {
+        CHECK(same_bits(s_ref.layers[i].weight_diff, s_gpu.layers[i].weight_diff), "weight_diff");
+        CHECK(same_bits(s_ref.layers[i].bias_diff, s_gpu.layers[i].bias_diff), "bias_diff");
+      }
+      sgd_step(s_ref, cfg);
+      gpu::sgd_step(got, cfg);
+      for (std::size_t i = 0; i < spec.layers.size(); ++i) {
+        CHECK(same_bits(s_ref.layers[i].weights, s_gpu.layers[i].weights), "sgd weights");
+        CHECK(same_bits(s_ref.layers[i].bias, s_gpu.layers[i].bias), "sgd bias");
+        CHECK(same_bits(s_ref.layers[i].weight_mom, s_gpu.layers[i].weight_mom), "sgd momentum");
+      }
+    }
+    // a diff seeded at the probability blob (softmax_backward)
+    Blob<float> x(spec.f0, spec.w0, spec.w0);
+    fill(x.data, rng);
+    ref.forward(x);
+    got.forward(x);
+    const std::string prob = spec.layers.back().output;
+    std::vector<float> seed(ref.blob(prob).size());
+    fill(seed, rng);
+    ref.blob_mut(prob).diff = seed;
+    got.blob_mut(prob).diff = seed;
+    ref.backward();
+    got.backward();
+    for (const auto& l : spec.layers)
+      CHECK(same_bits(ref.blob(l.output).diff, got.blob_mut(l.output).diff), "seeded backward diff");
+  }
+}
+
 int main() {
+  train_cases();
   conv_cases<float>();
   conv_cases<double>();
   layer_cases();
