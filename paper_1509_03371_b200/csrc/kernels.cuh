@@ -80,6 +80,13 @@ void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long l
 void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long long sak,
                       const float* b, long long sbk, long long sbj, double alpha, double beta,
                       float* c, cudaStream_t st);
+// f64-operand variant: 4-stage cp.async DMMA GEMM for problems that fill the GPU, else the
+// shape-adaptive kernel. a_k_contig: A(i,kk) = a[i*lda + kk], else a[kk*lda + i]; likewise B
+// with B(kk,j) = b[j*ldb + kk] (k contiguous) or b[kk*ldb + j].
+void gemm_dmma_f64ops(int m, int n, int k, const double* a, bool a_k_contig, long long lda,
+                      const double* b, bool b_k_contig, long long ldb, double alpha, double beta,
+                      float* c, cudaStream_t st);
+void widen_f32(const float* in, long long n, double* out, cudaStream_t st);
 void im2col_pitched(const double* in, int C, int H, int W, int wp, int k, int d, int s, int p,
                     int OH, int OW, double* col, cudaStream_t st);
 void bias_grad(const float* dout, int M, int n, float* bdiff, cudaStream_t st);

@@ -91,7 +91,7 @@ struct graft_net {
   int tile_batch = 0;
   bool keep_blobs = false;
   bool training = false;  // forward records pool argmax (LayerState::argmax) for backward
-  DevBuf col, col_grad, loss_terms, loss_dev;  // backward / softmax_loss scratch
+  DevBuf col, col_grad, loss_terms, loss_dev, dy64, w64;  // backward / softmax_loss scratch
   int retile_cap = 1024;  // largest internal process() tile (0: use the caller's tile)
   int last_tile = 0;      // internal tile used by the last process call
   int tc_kind = 0;        // tolerance mode: 0 = exact (default), TC_BF16 / TC_TF32 = eligible
@@ -890,13 +890,22 @@ void backward_impl(graft_net& n) {
           n.col.ensure(std::max<size_t>(static_cast<size_t>(fan_in) * npx, 1) * sizeof(double));
           im2col_pitched(in.buf.as<double>(), in.C, in.H, in.W, in.Wp, l.k, l.d, l.s, l.p, OH, OW,
                          n.col.as<double>(), n.stream);
-          gemm_dmma_f32out(l.f_out, fan_in, npx, dout, npx, 1, n.col.as<double>(), 1, npx, 1.0, 1.0,
-                           l.w_diff.as<float>(), n.stream);
+          // f64 copies of dOut and W so both GEMMs stream f64 operands with cp.async
+          const size_t ndy = static_cast<size_t>(l.f_out) * npx;
+          n.dy64.ensure(std::max<size_t>(ndy, 1) * sizeof(double));
+          widen_f32(dout, static_cast<long long>(ndy), n.dy64.as<double>(), n.stream);
+          // dW += dOut * col^T: A(i=f, kk=p) = dy[f][p], B(kk=p, j=r) = col[r][p]
+          gemm_dmma_f64ops(l.f_out, fan_in, npx, n.dy64.as<double>(), true, npx, n.col.as<double>(),
+                           true, npx, 1.0, 1.0, l.w_diff.as<float>(), n.stream);
           bias_grad(dout, l.f_out, npx, l.b_diff.as<float>(), n.stream);
           if (l.inputs[0] != "data") {
+            const size_t nw = static_cast<size_t>(l.f_out) * fan_in;
+            n.w64.ensure(std::max<size_t>(nw, 1) * sizeof(double));
+            widen_f32(l.w_f32.as<float>(), static_cast<long long>(nw), n.w64.as<double>(), n.stream);
             n.col_grad.ensure(std::max<size_t>(static_cast<size_t>(fan_in) * npx, 1) * sizeof(float));
-            gemm_dmma_f32out(fan_in, npx, l.f_out, l.w_f32.as<float>(), 1, fan_in, dout, npx, 1, 1.0,
-                             0.0, n.col_grad.as<float>(), n.stream);
+            // col_grad = W^T * dOut: A(i=r, kk=f) = W[f][r], B(kk=f, j=p) = dy[f][p]
+            gemm_dmma_f64ops(fan_in, npx, l.f_out, n.w64.as<double>(), false, fan_in,
+                             n.dy64.as<double>(), false, npx, 1.0, 0.0, n.col_grad.as<float>(), n.stream);
             col2im_add(n.col_grad.as<float>(), in.C, in.H, in.W, l.k, l.d, l.s, l.p, OH, OW, din,
                        n.stream);
           }
