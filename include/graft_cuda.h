@@ -181,6 +181,11 @@ int graft_process(graft_net* net, const uint8_t* img, int H, int W, int w, int v
  * [graft_band_rows(...)] -- the data-parallel unit of the multi-GPU partitioner. */
 int graft_process_band(graft_net* net, const uint8_t* img, int H, int W, int w, int v,
                        int row_begin, int row_end, uint8_t* labels, float* probs, int mem);
+/* process() of n_images same-size images stored back to back (img [N][H][W], labels [N][H][W],
+ * probs [N][C][H][W]): the tiles of all images share launches, so small images run at the
+ * large-image rate. Planes are bit-identical to N separate process() calls. */
+int graft_process_batch(graft_net* net, const uint8_t* imgs, int n_images, int H, int W, int w,
+                        int v, uint8_t* labels, float* probs, int mem);
 /* Number of tile rows process() visits for extent H and tile w, and the output row range
  * [*y0, *y1) owned by tile rows [row_begin, row_end) (disjoint across a partition). */
 int graft_tile_rows(int H, int w, int* n_rows);

@@ -116,6 +116,7 @@ _SIGS = {
     "graft_net_stream": (_vp, [_vp]),
     "graft_fp64_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _i]),
+    "graft_process_batch": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _i]),
     "graft_process_band": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _i]),
     "graft_tile_rows": (_i, [_i, _i, _pi]),
     "graft_band_rows": (_i, [_i, _i, _i, _i, _pi, _pi]),

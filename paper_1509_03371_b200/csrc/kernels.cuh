@@ -142,12 +142,15 @@ void normalize_u8(const uint8_t* img, size_t n, float* out, cudaStream_t st);
 // W - w)), the edge-snapping tile_offsets lambda (pipeline.hpp:662-672) started at y_base.
 // Builds the inputs of tiles [t0, t0 + n_tiles) as n_tiles x f0 x (w+v) x (w+v) widened f32:
 // mirror_pad + normalize_image + the f0-channel copy, straight from the raw u8 image.
+// tiles_per_image > 0: a batch of same-size images stored back to back ([N][H][W]); global
+// tile t belongs to image t / tiles_per_image.
 void build_tiles(const uint8_t* img, int H, int W, int v, int w, int ntx, int t0, int n_tiles,
-                 int f0, double* out, cudaStream_t st, int wp = 0, int y_base = 0);
+                 int f0, double* out, cudaStream_t st, int wp = 0, int y_base = 0,
+                 int tiles_per_image = 0);
 // Softmax head + per-pixel argmax + stitch of the tiles' scores (n_tiles x C x w x w) into the
 // image planes: labels H x W (u8), probs C x H x W (f32); rows outside [y_lo, y_hi) skipped.
 void softmax_stitch(const double* scores, int n_tiles, int C, int w, int ntx, int t0, int H, int W,
                     int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st, int wp = 0,
-                    int y_base = 0);
+                    int y_base = 0, int tiles_per_image = 0);
 
 }  // namespace graft

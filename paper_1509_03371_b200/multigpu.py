@@ -116,3 +116,54 @@ def gather_batch(per_image: dict, n_images: int, shape_lab, shape_prob, rank: in
             if i + r < n_images:
                 labs[i + r], probs[i + r] = la[r], pa[r]
     return labs, probs
+
+
+def shard_range(n_images: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous block of a batch owned by `rank` (sizes differ by at most one)."""
+    q, r = divmod(n_images, world)
+    begin = rank * q + min(rank, r)
+    return begin, begin + q + (1 if rank < r else 0)
+
+
+def gather_shards(lab_shard, prob_shard, n_images: int, rank: int, world: int, group=None):
+    """All-gathers per-rank batch shards (labels [n_r, H, W], probs [n_r, C, H, W], rank r owning
+    shard_range(...)) into the full batch on every rank: the batch mode's only collective.
+    Shards are padded to the largest size for the NCCL all-gather and trimmed after."""
+    import torch
+    import torch.distributed as dist
+
+    sizes = [shard_range(n_images, world, r) for r in range(world)]
+    cap = max(e - b for b, e in sizes)
+
+    def padded(t):
+        out = torch.zeros((cap,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        out[:t.shape[0]] = t
+        return out
+
+    lp, pp = padded(lab_shard), padded(prob_shard)
+    if world > 1:
+        la = [torch.empty_like(lp) for _ in range(world)]
+        pa = [torch.empty_like(pp) for _ in range(world)]
+        dist.all_gather(la, lp, group=group)
+        dist.all_gather(pa, pp, group=group)
+    else:
+        la, pa = [lp], [pp]
+    labs = torch.cat([la[r][:e - b] for r, (b, e) in enumerate(sizes)])
+    probs = torch.cat([pa[r][:e - b] for r, (b, e) in enumerate(sizes)])
+    return labs, probs
+
+
+def process_batch_sharded(proc, images, w: int, v: int, rank: int, world: int, device,
+                          group=None):
+    """Weak-scaling batch mode (BASELINE configs[3]): rank r runs graft_process_batch on its
+    contiguous shard of the (N, H, W) device batch and the shards are all-gathered."""
+    import torch
+    from . import _lib
+
+    n, H, W = images.shape
+    b, e = shard_range(n, world, rank)
+    lab = torch.empty((e - b, H, W), dtype=torch.uint8, device=device)
+    prob = torch.empty((e - b, proc.n_classes, H, W), dtype=torch.float32, device=device)
+    if e > b:
+        proc.run_batch(images[b:e], w, v, lab, prob, mem=_lib.MEM_DEVICE)
+    return gather_shards(lab, prob, n, rank, world, group)

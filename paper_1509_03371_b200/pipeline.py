@@ -113,6 +113,23 @@ class Processor:
         return labels, probs
 
 
+    def run_batch(self, images, w: int, v: int, labels=None, probs=None, mem: int = 0):
+        """process() of N same-size images (N, H, W) in shared launches -> labels (N, H, W) u8,
+        probs (N, C, H, W) f32, bit-identical to N separate run() calls."""
+        if mem == _lib.MEM_HOST:
+            images = np.ascontiguousarray(images, np.uint8)
+            N, H, W = images.shape
+            if labels is None:
+                labels = np.zeros((N, H, W), np.uint8)
+            if probs is None:
+                probs = np.zeros((N, self.n_classes, H, W), np.float32)
+        else:
+            N, H, W = images.shape
+        self.net.sync_params(self.spec, self.states)
+        _lib.check(_lib.lib().graft_process_batch(self.net.h, _lib.ptr(images), N, H, W, w, v,
+                                                  _lib.ptr(labels), _lib.ptr(probs), mem))
+        return labels, probs
+
     def last_tile(self) -> int:
         """Internal tile size the last run() used."""
         import ctypes as C

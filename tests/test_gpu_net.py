@@ -210,3 +210,32 @@ def test_process_single_tile_equals_forward():
     x = np.ascontiguousarray(np.broadcast_to(padded, (3, 229, 229)))
     out = g.NetRunner(spec, states).forward(g.Blob.from_array(x)).view()
     assert_bitwise(np.stack([p.view() for p in res.probs]), out, "process vs forward")
+
+
+def test_process_batch_equals_separate_images(gnets):
+    """graft_process_batch (BASELINE configs[3]: a batch of independent images): the tiles of all
+    images share launches; every image's planes equal its own process() bit for bit, including
+    the reference's own tiled-inference fixture (test_pipeline.cpp:535-588) as a batch member."""
+    spec = spec_of(gnets, "tile_spec")
+    states = g.init_weights(spec, 17)
+    proc = g.Processor(spec, states, tile_batch=3)  # batches straddle image boundaries
+    base = gnets["tile_img"]
+    imgs = np.stack([base] + [g.Rng(90 + i).index_array_u8(base.size, 256).reshape(base.shape)
+                              for i in range(4)])
+    labs, probs = proc.run_batch(imgs, 8, 5)
+    assert np.array_equal(labs[0], gnets["tile_w8_labels"])
+    assert_bitwise(probs[0], gnets["tile_w8_probs"], "batch member 0 vs reference fixture")
+    for i in range(len(imgs)):
+        lab, pr = proc.run(imgs[i], 8, 5)
+        assert np.array_equal(labs[i], lab)
+        assert_bitwise(probs[i], pr, f"batch member {i}")
+    # full sk.net, 3 images of 200x180 (internal retiling applies per image)
+    spec = g.parse_netspec_or_throw(config_text("sk.net"))
+    states = g.init_weights(spec, 1)
+    proc = g.Processor(spec, states)
+    imgs = np.stack([g.Rng(7 + i).index_array_u8(200 * 180, 256).reshape(200, 180) for i in range(3)])
+    labs, probs = proc.run_batch(imgs, 128, 101)
+    for i in range(3):
+        lab, pr = proc.run(imgs[i], 128, 101)
+        assert np.array_equal(labs[i], lab)
+        assert_bitwise(probs[i], pr, f"sk batch member {i}")

@@ -36,6 +36,15 @@ def test_split_rows_and_bands_cover_exactly():
             assert (covered == 1).all(), (H, w, world, bands)
 
 
+def test_shard_range_covers_exactly():
+    for n in (0, 1, 5, 64, 67):
+        for world in (1, 2, 3, 8):
+            spans = [M.shard_range(n, world, r) for r in range(world)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+            assert max(e - b for b, e in spans) - min(e - b for b, e in spans) <= 1
+
+
 def _worker(rank, world, port, H, W, w, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -69,6 +78,13 @@ def _worker(rank, world, port, H, W, w, q):
         per[i] = (torch.full((4, 5), i, dtype=torch.uint8), torch.full((2, 4, 5), float(i)))
     labs, prs = M.gather_batch(per, 3, (4, 5), (2, 4, 5), rank, world, "cpu")
     ok = ok and all(int(labs[i][0, 0]) == i and float(prs[i][1, 3, 4]) == i for i in range(3))
+    # sharded batch mode (graft_process_batch per rank + one all-gather): 5 images over 2 ranks
+    b, e = M.shard_range(5, world, rank)
+    lab_sh = torch.stack([torch.full((4, 5), i, dtype=torch.uint8) for i in range(b, e)])
+    prob_sh = torch.stack([torch.full((2, 4, 5), float(i) + 0.5) for i in range(b, e)])
+    la, pa = M.gather_shards(lab_sh, prob_sh, 5, rank, world)
+    ok = ok and la.shape == (5, 4, 5) and all(int(la[i, 3, 4]) == i for i in range(5)) and \
+        all(float(pa[i, 1, 0, 0]) == i + 0.5 for i in range(5))
     q.put((rank, ok))
     dist.destroy_process_group()
 
