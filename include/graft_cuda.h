@@ -226,6 +226,37 @@ int graft_net_set_param_state_f32(graft_net* net, int layer, int which, const fl
 int graft_net_softmax_loss_f32(graft_net* net, const char* scores_blob, const int32_t* labels,
                                const uint8_t* mask, int H, int W, double* loss);
 int graft_net_sgd_step(graft_net* net, double lr, double momentum, double weight_decay);
+
+/* Layer-level backward API (S = float), the reference's functions one for one. Arguments the
+ * reference accumulates into (`diff +=`) are read and written: dweights/dbias
+ * (LayerState::weight_diff/bias_diff), din (in.diff). */
+/* conv_sk_backward (layers.hpp:68-95); din NULL = propagate_input false. */
+int graft_conv_sk_backward_f32(const float* in, int C, int H, int W, const float* weights, int f_out,
+                               int k, int d, int s, int p, const float* dout, float* dweights,
+                               float* dbias, float* din, int mem);
+/* col2im_sk (tensor.hpp:113-145): out (C x H x W) = scatter of col (C*k*k x OH*OW). */
+int graft_col2im_sk_f32(const float* col, int C, int H, int W, int k, int d, int s, int p, float* out,
+                        int mem);
+/* maxpool_sk_backward (layers.hpp:134-139): din[argmax[o]] += dout[o], o ascending. With the
+ * forward's geometry (k > 0) the device gathers per window; k <= 0 (any argmax table) runs the
+ * reference's scatter in o order. Indices outside the C x H x W input: SizeError. */
+int graft_maxpool_sk_backward_f32(const uint64_t* argmax, const float* dout, size_t n_out, int C,
+                                  int H, int W, int k, int d, int s, float* din, int mem);
+int graft_relu_backward_f32(const float* in_data, const float* dout, size_t n, float* din, int mem);
+/* upconv_backward (layers.hpp:178-190); C, H, W of the input (dout is C x 2H x 2W). */
+int graft_upconv_backward_f32(const float* dout, int C, int H, int W, float* din, int mem);
+/* mergecrop_backward (layers.hpp:214-221): da += the first Ca channels of dout. */
+int graft_mergecrop_backward_f32(const float* dout, int Ca, int H, int W, float* da, int mem);
+/* softmax_backward (layers.hpp:246-262): din += J^T dout, out_data = the softmax output. */
+int graft_softmax_backward_f32(const float* out_data, const float* dout, int C, int H, int W,
+                               float* din, int mem);
+/* softmax_loss (layers.hpp:269-307) on a score blob: dscores += gradient, *loss = the loss;
+ * labels H x W int32 and mask H x W u8 (or NULL) are host planes. */
+int graft_softmax_loss_layer_f32(const float* scores, int C, int H, int W, const int32_t* labels,
+                                 const uint8_t* mask, float* dscores, double* loss, int mem);
+/* sgd_step (pipeline.hpp:483-500) on one parameter array. */
+int graft_sgd_step_f32(float* w, float* mom, float* diff, size_t n, double lr, double momentum,
+                       double weight_decay, int mem);
 int graft_net_get_option(const graft_net* net, int option, long long* value);
 
 /* ---- host-only Rng (rng.hpp:12-54): std::mt19937_64 + the reference's transforms ----------

@@ -99,6 +99,15 @@ _REF_SIGS = {
     "ref_net_param_state": (None, [_vp, _i, _i, _vp, _vp]),
     "ref_net_softmax_loss": (_i, [_vp, C.c_char_p, _vp, _vp, _i, _i, C.POINTER(_d)]),
     "ref_net_sgd_step": (_i, [_vp, _d, _d, _d]),
+    "ref_conv_backward_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp]),
+    "ref_col2im_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp]),
+    "ref_maxpool_backward_f32": (_i, [_vp, _vp, _i, _i, _i, _i, _vp]),
+    "ref_relu_backward_f32": (None, [_vp, _vp, _i, _vp]),
+    "ref_upconv_backward_f32": (None, [_vp, _i, _i, _i, _vp]),
+    "ref_mergecrop_backward_f32": (None, [_vp, _i, _i, _i, _i, _vp]),
+    "ref_softmax_backward_f32": (None, [_vp, _vp, _i, _i, _i, _vp]),
+    "ref_softmax_loss_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d)]),
+    "ref_sgd_step_f32": (None, [_vp, _vp, _vp, _i, _d, _d, _d]),
     "ref_write_pgm": (_i, [C.c_char_p, _vp, _i, _i]),
 }
 

@@ -384,4 +384,119 @@ int ref_net_sgd_step(void* h, double lr, double momentum, double weight_decay) {
   });
 }
 
+// ---- layer-level backward functions (test_layers.cpp:107-389) ----
+int ref_conv_backward_f32(const float* in, int C, int H, int W, const float* w, int f_out, int k, int d,
+                          int s, int p, const float* dout, float* dw, float* db, float* din) {
+  return guard([&] {
+    Blob<float> x = make_blob(in, C, H, W);
+    const ConvGeometry g = ConvGeometry::from_input(k, d, s, p, H, W);
+    LayerState<float> st;
+    st.init_conv(f_out, C * k * k);
+    std::memcpy(st.weights.data(), w, sizeof(float) * st.weights.size());
+    std::memcpy(st.weight_diff.data(), dw, sizeof(float) * st.weight_diff.size());
+    std::memcpy(st.bias_diff.data(), db, sizeof(float) * st.bias_diff.size());
+    if (din) x.diff.assign(din, din + x.size());
+    Blob<float> out(f_out, g.out_h, g.out_w);
+    out.diff.assign(dout, dout + out.size());
+    ColumnBuffer<float> cb, cg;
+    conv_sk_backward(x, st, f_out, g, cb, cg, out, din != nullptr);
+    std::memcpy(dw, st.weight_diff.data(), sizeof(float) * st.weight_diff.size());
+    std::memcpy(db, st.bias_diff.data(), sizeof(float) * st.bias_diff.size());
+    if (din) std::memcpy(din, x.diff.data(), sizeof(float) * x.size());
+  });
+}
+
+int ref_col2im_f32(const float* col, int C, int H, int W, int k, int d, int s, int p, float* out) {
+  return guard([&] {
+    const ConvGeometry g = ConvGeometry::from_input(k, d, s, p, H, W);
+    ColumnBuffer<float> cb;
+    cb.resize(C * k * k, g.out_h * g.out_w);
+    std::memcpy(cb.data.data(), col, sizeof(float) * cb.rows * cb.cols);
+    Blob<float> o;
+    col2im_sk(cb, g, C, o);
+    std::memcpy(out, o.data.data(), sizeof(float) * o.size());
+  });
+}
+
+int ref_maxpool_backward_f32(const uint64_t* argmax, const float* dout, int n_out, int C, int H, int W,
+                             float* din) {
+  return guard([&] {
+    Blob<float> x(C, H, W);
+    x.diff.assign(din, din + x.size());
+    LayerState<float> st;
+    st.argmax.assign(argmax, argmax + n_out);
+    Blob<float> out(1, 1, n_out);
+    out.diff.assign(dout, dout + n_out);
+    maxpool_sk_backward(x, st, out);
+    std::memcpy(din, x.diff.data(), sizeof(float) * x.size());
+  });
+}
+
+void ref_relu_backward_f32(const float* in, const float* dout, int n, float* din) {
+  Blob<float> x(1, 1, n), out(1, 1, n);
+  std::memcpy(x.data.data(), in, sizeof(float) * n);
+  x.diff.assign(din, din + n);
+  out.diff.assign(dout, dout + n);
+  relu_backward(x, out);
+  std::memcpy(din, x.diff.data(), sizeof(float) * n);
+}
+
+void ref_upconv_backward_f32(const float* dout, int C, int H, int W, float* din) {
+  Blob<float> x(C, H, W), out(C, 2 * H, 2 * W);
+  x.diff.assign(din, din + x.size());
+  out.diff.assign(dout, dout + out.size());
+  upconv_backward(x, out);
+  std::memcpy(din, x.diff.data(), sizeof(float) * x.size());
+}
+
+void ref_mergecrop_backward_f32(const float* dout, int Ca, int Cb, int H, int W, float* da) {
+  Blob<float> a(Ca, H, W), out(Ca + Cb, H, W);
+  a.diff.assign(da, da + a.size());
+  out.diff.assign(dout, dout + out.size());
+  mergecrop_backward(a, out);
+  std::memcpy(da, a.diff.data(), sizeof(float) * a.size());
+}
+
+void ref_softmax_backward_f32(const float* out_data, const float* dout, int C, int H, int W, float* din) {
+  Blob<float> x(C, H, W), out(C, H, W);
+  std::memcpy(out.data.data(), out_data, sizeof(float) * out.size());
+  out.diff.assign(dout, dout + out.size());
+  x.diff.assign(din, din + x.size());
+  softmax_backward(x, out);
+  std::memcpy(din, x.diff.data(), sizeof(float) * x.size());
+}
+
+int ref_softmax_loss_f32(const float* scores, int C, int H, int W, const int* labels, const uint8_t* mask,
+                         float* dscores, double* loss) {
+  return guard([&] {
+    Blob<float> s = make_blob(scores, C, H, W);
+    s.diff.assign(dscores, dscores + s.size());
+    Plane<int> lab(H, W);
+    std::memcpy(lab.pix.data(), labels, sizeof(int) * lab.size());
+    Plane<std::uint8_t> m;
+    if (mask) {
+      m = Plane<std::uint8_t>(H, W);
+      std::memcpy(m.pix.data(), mask, m.size());
+    }
+    *loss = softmax_loss(s, lab, m);
+    if (s.diff.size() == s.size()) std::memcpy(dscores, s.diff.data(), sizeof(float) * s.size());
+  });
+}
+
+void ref_sgd_step_f32(float* w, float* mom, float* diff, int n, double lr, double momentum, double wd) {
+  NetStates<float> st;
+  st.layers.resize(1);
+  st.layers[0].weights.assign(w, w + n);
+  st.layers[0].weight_mom.assign(mom, mom + n);
+  st.layers[0].weight_diff.assign(diff, diff + n);
+  SolverConfig cfg;
+  cfg.lr = lr;
+  cfg.momentum = momentum;
+  cfg.weight_decay = wd;
+  sgd_step(st, cfg);
+  std::memcpy(w, st.layers[0].weights.data(), sizeof(float) * n);
+  std::memcpy(mom, st.layers[0].weight_mom.data(), sizeof(float) * n);
+  std::memcpy(diff, st.layers[0].weight_diff.data(), sizeof(float) * n);
+}
+
 }  // extern "C"

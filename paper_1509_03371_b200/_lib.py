@@ -137,6 +137,15 @@ _SIGS = {
     "graft_net_set_param_state_f32": (_i, [_vp, _i, _i, _vp, _vp]),
     "graft_net_softmax_loss_f32": (_i, [_vp, C.c_char_p, _vp, _vp, _i, _i, C.POINTER(_d)]),
     "graft_net_sgd_step": (_i, [_vp, _d, _d, _d]),
+    "graft_conv_sk_backward_f32": (_i, [_vp, _i, _i, _i, _vp, _i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _i]),
+    "graft_col2im_sk_f32": (_i, [_vp, _i, _i, _i, _i, _i, _i, _i, _vp, _i]),
+    "graft_maxpool_sk_backward_f32": (_i, [_vp, _vp, _sz, _i, _i, _i, _i, _i, _i, _vp, _i]),
+    "graft_relu_backward_f32": (_i, [_vp, _vp, _sz, _vp, _i]),
+    "graft_upconv_backward_f32": (_i, [_vp, _i, _i, _i, _vp, _i]),
+    "graft_mergecrop_backward_f32": (_i, [_vp, _i, _i, _i, _vp, _i]),
+    "graft_softmax_backward_f32": (_i, [_vp, _vp, _i, _i, _i, _vp, _i]),
+    "graft_softmax_loss_layer_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d), _i]),
+    "graft_sgd_step_f32": (_i, [_vp, _vp, _vp, _sz, _d, _d, _d, _i]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),
 }

@@ -33,6 +33,14 @@ class Blob:
         self.data = np.zeros(f * h * w, self.dtype)
         self.diff = np.zeros(0, self.dtype)
 
+    def ensure_diff(self) -> None:
+        """Blob::ensure_diff (blob.hpp:43-45): a diff of the wrong size becomes zeros."""
+        if self.diff.size != self.size():
+            self.diff = np.zeros(self.size(), self.dtype)
+
+    def zero_diff(self) -> None:
+        self.diff = np.zeros(self.size(), self.dtype)
+
     def plane(self) -> int:
         return self.height * self.width
 

@@ -94,6 +94,12 @@ void col2im_add(const float* colg, int C, int H, int W, int k, int d, int s, int
                 float* diff, cudaStream_t st);
 void maxpool_backward(const uint64_t* argmax, const float* dout, int C, int H, int W, int k, int d,
                       int s, int OH, int OW, float* din, cudaStream_t st);
+// API form: any argmax table (indices outside their window fall back to the reference's
+// serial scatter; indices outside the input throw SizeError).
+void maxpool_backward_checked(const uint64_t* argmax, const float* dout, int C, int H, int W, int k,
+                              int d, int s, int OH, int OW, float* din, size_t n_in, cudaStream_t st);
+void maxpool_backward_scatter(const uint64_t* argmax, const float* dout, long long n_out, float* din,
+                             size_t n_in, cudaStream_t st);
 void relu_backward(const double* data, int rows, int W, int wp, const float* dout, float* din,
                    cudaStream_t st);
 void upconv_backward(const float* dout, int C, int H, int W, float* din, cudaStream_t st);

@@ -136,3 +136,135 @@ def gemm(transpose_a: bool, transpose_b: bool, m: int, n: int, k: int, alpha, a:
 
 def gemm_flops(m: int, n: int, k: int) -> int:  # tensor.hpp:173-175
     return m * n * (2 * k - 1)
+
+
+# ---- backward functions, S = float ------------------------------------
+def _f32(dtype):
+    if np.dtype(dtype) != np.float32:
+        raise TypeError("the B200 backward path runs S=float")
+
+
+def conv_sk_backward(in_: Blob, state: LayerState, f_out: int, g: ConvGeometry, colbuf: ColumnBuffer,
+                     col_grad: ColumnBuffer, out: Blob, propagate_input: bool = True) -> None:
+    """conv_sk_backward (layers.hpp:68-95): dW += dOut col^T, db += row sums, in.diff +=
+    col2im(W^T dOut) (when propagate_input). Column buffers are accepted for signature parity."""
+    _f32(in_.dtype)
+    if out.diff.size != out.size():
+        raise SizeError("conv backward: output diff missing")
+    fan_in = in_.channels * g.k * g.k
+    if state.weights.size != f_out * fan_in:
+        raise SizeError(f"conv: weight count {state.weights.size} != f_out*f_in*k*k = {f_out * fan_in}")
+    if state.weight_diff.size != state.weights.size:
+        state.weight_diff = np.zeros(state.weights.size, np.float32)
+    if state.bias_diff.size != f_out:
+        state.bias_diff = np.zeros(f_out, np.float32)
+    if propagate_input:
+        in_.ensure_diff()
+    dw = _c(state.weight_diff, np.float32)
+    db = _c(state.bias_diff, np.float32)
+    din = _c(in_.diff, np.float32) if propagate_input else None
+    _lib.check(_lib.lib().graft_conv_sk_backward_f32(
+        _lib.ptr(_c(in_.data, np.float32)), in_.channels, in_.height, in_.width,
+        _lib.ptr(_c(state.weights, np.float32)), f_out, g.k, g.d, g.s, g.p,
+        _lib.ptr(_c(out.diff, np.float32)), _lib.ptr(dw), _lib.ptr(db), _lib.ptr(din), _H))
+    state.weight_diff, state.bias_diff = dw, db
+    if propagate_input:
+        in_.diff = din
+
+
+def col2im_sk(col: ColumnBuffer, g: ConvGeometry, channels: int, out: Blob) -> None:
+    """col2im_sk (tensor.hpp:113-145): out = the exact adjoint scatter of col."""
+    if col.rows != channels * g.k * g.k or col.cols != g.out_h * g.out_w:
+        raise SizeError(f"col2im_sk: column buffer is {col.rows}x{col.cols}, expected "
+                        f"{channels * g.k * g.k}x{g.out_h * g.out_w}")
+    out.resize(channels, g.in_h, g.in_w)
+    data = np.zeros(out.size(), np.float32)
+    _lib.check(_lib.lib().graft_col2im_sk_f32(_lib.ptr(_c(col.data[:col.rows * col.cols], np.float32)),
+                                              channels, g.in_h, g.in_w, g.k, g.d, g.s, g.p,
+                                              _lib.ptr(data), _H))
+    out.data = data
+
+
+def maxpool_sk_backward(in_: Blob, state: LayerState, out: Blob, g: ConvGeometry = None) -> None:
+    """maxpool_sk_backward (layers.hpp:134-139): in.diff[argmax[o]] += out.diff[o], o ascending.
+    With the forward's geometry `g` the device gathers per pooling window; without it any
+    argmax table is replayed in the reference's scatter order."""
+    _f32(in_.dtype)
+    if state.argmax is None or state.argmax.size != out.size():
+        raise SizeError("pool backward: stale argmax cache")
+    in_.ensure_diff()
+    din = _c(in_.diff, np.float32)
+    k, d, s = (g.k, g.d, g.s) if g is not None else (0, 1, 1)
+    _lib.check(_lib.lib().graft_maxpool_sk_backward_f32(
+        _lib.ptr(_c(state.argmax, np.uint64)), _lib.ptr(_c(out.diff, np.float32)), out.size(),
+        in_.channels, in_.height, in_.width, k, d, s, _lib.ptr(din), _H))
+    in_.diff = din
+
+
+def relu_backward(in_: Blob, out: Blob) -> None:
+    """relu_backward (layers.hpp:149-155): in.diff += out.diff where in.data > 0."""
+    _f32(in_.dtype)
+    in_.ensure_diff()
+    din = _c(in_.diff, np.float32)
+    _lib.check(_lib.lib().graft_relu_backward_f32(_lib.ptr(_c(in_.data, np.float32)),
+                                                  _lib.ptr(_c(out.diff, np.float32)), in_.size(),
+                                                  _lib.ptr(din), _H))
+    in_.diff = din
+
+
+def upconv_backward(in_: Blob, out: Blob) -> None:
+    """upconv_backward (layers.hpp:178-190)."""
+    _f32(in_.dtype)
+    in_.ensure_diff()
+    din = _c(in_.diff, np.float32)
+    _lib.check(_lib.lib().graft_upconv_backward_f32(_lib.ptr(_c(out.diff, np.float32)), in_.channels,
+                                                    in_.height, in_.width, _lib.ptr(din), _H))
+    in_.diff = din
+
+
+def mergecrop_backward(a: Blob, out: Blob) -> None:
+    """mergecrop_backward (layers.hpp:214-221): gradient into the first input only."""
+    _f32(a.dtype)
+    a.ensure_diff()
+    da = _c(a.diff, np.float32)
+    _lib.check(_lib.lib().graft_mergecrop_backward_f32(
+        _lib.ptr(_c(out.diff[:a.size()], np.float32)), a.channels, a.height, a.width,
+        _lib.ptr(da), _H))
+    a.diff = da
+
+
+def softmax_backward(in_: Blob, out: Blob) -> None:
+    """softmax_backward (layers.hpp:246-262): in.diff += J^T out.diff."""
+    _f32(in_.dtype)
+    in_.ensure_diff()
+    din = _c(in_.diff, np.float32)
+    _lib.check(_lib.lib().graft_softmax_backward_f32(_lib.ptr(_c(out.data, np.float32)),
+                                                     _lib.ptr(_c(out.diff, np.float32)), in_.channels,
+                                                     in_.height, in_.width, _lib.ptr(din), _H))
+    in_.diff = din
+
+
+def softmax_loss(scores: Blob, labels, mask=None) -> float:
+    """softmax_loss (layers.hpp:269-307): returns the loss, scores.diff += gradient. labels: int
+    plane (H, W); mask: u8 plane or None (all pixels count)."""
+    import ctypes as C
+
+    _f32(scores.dtype)
+    lab = np.ascontiguousarray(getattr(labels, "pix", labels), np.int32).reshape(-1)
+    if lab.size != scores.plane():
+        raise SizeError(f"softmax_loss: label plane does not match scores")
+    m = None
+    if mask is not None:
+        m = np.ascontiguousarray(getattr(mask, "pix", mask), np.uint8).reshape(-1)
+        if m.size == 0:
+            m = None
+        elif m.size != scores.plane():
+            raise SizeError("softmax_loss: mask plane does not match scores")
+    scores.ensure_diff()
+    d = _c(scores.diff, np.float32)
+    loss = C.c_double()
+    _lib.check(_lib.lib().graft_softmax_loss_layer_f32(
+        _lib.ptr(_c(scores.data, np.float32)), scores.channels, scores.height, scores.width,
+        _lib.ptr(lab), _lib.ptr(m), _lib.ptr(d), C.byref(loss), _H))
+    scores.diff = d
+    return loss.value

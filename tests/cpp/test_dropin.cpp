@@ -248,8 +248,121 @@ static void train_cases() {
   }
 }
 
+// Layer-level backward functions (test_layers.cpp:107-389) vs the drop-ins.
+static void backward_layer_cases() {
+  Rng rng(41);
+  struct Case { int f_in, f_out, h, w, k, d, s, p; };
+  const Case cases[] = {{3, 4, 9, 9, 3, 1, 1, 0}, {2, 5, 11, 11, 3, 2, 1, 0}, {4, 2, 8, 8, 2, 1, 2, 0},
+                        {2, 2, 6, 6, 3, 1, 1, 1}, {12, 130, 40, 40, 10, 3, 1, 0}};
+  for (const auto& c : cases) {
+    const ConvGeometry g = ConvGeometry::from_input(c.k, c.d, c.s, c.p, c.h, c.w);
+    Blob<float> in1(c.f_in, c.h, c.w);
+    fill(in1.data, rng);
+    in1.ensure_diff();
+    fill(in1.diff, rng);
+    Blob<float> in2 = in1;
+    LayerState<float> s1;
+    s1.init_conv(c.f_out, c.f_in * c.k * c.k);
+    fill(s1.weights, rng);
+    fill(s1.weight_diff, rng);
+    fill(s1.bias_diff, rng);
+    LayerState<float> s2 = s1;
+    Blob<float> out(c.f_out, g.out_h, g.out_w);
+    out.ensure_diff();
+    fill(out.diff, rng);
+    ColumnBuffer<float> cb, cg;
+    conv_sk_backward(in1, s1, c.f_out, g, cb, cg, out, true);
+    gpu::conv_sk_backward(in2, s2, c.f_out, g, cb, cg, out, true);
+    CHECK(same_bits(s1.weight_diff, s2.weight_diff), "conv_sk_backward dW");
+    CHECK(same_bits(s1.bias_diff, s2.bias_diff), "conv_sk_backward db");
+    CHECK(same_bits(in1.diff, in2.diff), "conv_sk_backward din");
+    ColumnBuffer<float> col;
+    col.resize(c.f_in * c.k * c.k, g.out_h * g.out_w);
+    fill(col.data, rng);
+    Blob<float> o1, o2;
+    col2im_sk(col, g, c.f_in, o1);
+    gpu::col2im_sk(col, g, c.f_in, o2);
+    CHECK(same_bits(o1.data, o2.data), "col2im_sk");
+  }
+  {  // pooling with ties, then backward through the argmax
+    Blob<float> x(3, 13, 13);
+    for (auto& v : x.data) v = static_cast<float>(static_cast<int>(rng.uniform(0.0, 4.0))) * 0.5f;
+    const ConvGeometry g = ConvGeometry::from_input(2, 2, 1, 0, 13, 13);
+    LayerState<float> st;
+    Blob<float> y;
+    maxpool_sk_forward(x, st, g, y);
+    y.ensure_diff();
+    fill(y.diff, rng);
+    Blob<float> a = x, b = x;
+    a.ensure_diff();
+    fill(a.diff, rng);
+    b.diff = a.diff;
+    maxpool_sk_backward(a, st, y);
+    gpu::maxpool_sk_backward(b, st, y);
+    CHECK(same_bits(a.diff, b.diff), "maxpool_sk_backward");
+    Blob<float> r1 = x, r2 = x, ro(3, 13, 13);
+    ro.ensure_diff();
+    fill(ro.diff, rng);
+    relu_backward(r1, ro);
+    gpu::relu_backward(r2, ro);
+    CHECK(same_bits(r1.diff, r2.diff), "relu_backward");
+    Blob<float> u1(3, 6, 7), u2(3, 6, 7), uo(3, 12, 14);
+    uo.ensure_diff();
+    fill(uo.diff, rng);
+    upconv_backward(u1, uo);
+    gpu::upconv_backward(u2, uo);
+    CHECK(same_bits(u1.diff, u2.diff), "upconv_backward");
+    Blob<float> m1(2, 5, 5), m2(2, 5, 5), mo(5, 5, 5);
+    mo.ensure_diff();
+    fill(mo.diff, rng);
+    mergecrop_backward(m1, mo);
+    gpu::mergecrop_backward(m2, mo);
+    CHECK(same_bits(m1.diff, m2.diff), "mergecrop_backward");
+    Blob<float> sc(3, 4, 5), pr;
+    fill(sc.data, rng);
+    softmax_forward(sc, pr);
+    pr.ensure_diff();
+    fill(pr.diff, rng);
+    Blob<float> s1 = sc, s2 = sc;
+    softmax_backward(s1, pr);
+    gpu::softmax_backward(s2, pr);
+    CHECK(same_bits(s1.diff, s2.diff), "softmax_backward");
+    Plane<int> lab(4, 5);
+    for (auto& v : lab.pix) v = static_cast<int>(rng.uniform_index(3));
+    Plane<std::uint8_t> mask(4, 5, 1);
+    Blob<float> l1 = sc, l2 = sc;
+    const double a1 = softmax_loss(l1, lab, mask), a2 = gpu::softmax_loss(l2, lab, mask);
+    CHECK(std::memcmp(&a1, &a2, sizeof a1) == 0 && same_bits(l1.diff, l2.diff), "softmax_loss (layer)");
+  }
+  {  // sgd_step over NetStates (test_pipeline.cpp:336-395)
+    const NetSpec spec = parse_netspec_or_throw(
+        "input w=8 f=1\nlayer c1 conv_sk k=3 fout=4 in=data out=c1 init=he\n"
+        "layer prob softmax_loss in=c1 out=prob\n");
+    NetStates<float> a = init_weights<float>(spec, 5);
+    for (auto& st : a.layers) {
+      fill(st.weight_diff, rng);
+      fill(st.weight_mom, rng);
+      fill(st.bias_diff, rng);
+    }
+    NetStates<float> b = a;
+    SolverConfig cfg;
+    cfg.lr = 0.03;
+    cfg.momentum = 0.8;
+    cfg.weight_decay = 1e-3;
+    sgd_step(a, cfg);
+    gpu::sgd_step(b, cfg);
+    for (std::size_t i = 0; i < a.layers.size(); ++i) {
+      CHECK(same_bits(a.layers[i].weights, b.layers[i].weights), "sgd_step weights");
+      CHECK(same_bits(a.layers[i].weight_mom, b.layers[i].weight_mom), "sgd_step momentum");
+      CHECK(same_bits(a.layers[i].weight_diff, b.layers[i].weight_diff), "sgd_step diff");
+      CHECK(same_bits(a.layers[i].bias, b.layers[i].bias), "sgd_step bias");
+    }
+  }
+}
+
 int main() {
   train_cases();
+  backward_layer_cases();
   conv_cases<float>();
   conv_cases<double>();
   layer_cases();
