@@ -56,6 +56,8 @@ struct TcArgs {
   int nseg;            // ceil(OW / BN)
   int relu;            // apply relu to `out`
   int out_f64;
+  void* out_nhwc;      // optional: relu(conv) as the NEXT tc conv's operand, [B][OH][OW][nhwc_c]
+  int nhwc_c;          // channel stride of out_nhwc (f_out padded to the K block)
 };
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -94,6 +96,19 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* tm, int x, 
       "{%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
       "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
       : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T to_tc(float x);
+template <>
+__device__ __forceinline__ __nv_bfloat16 to_tc<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+template <>
+__device__ __forceinline__ float to_tc<float>(float x) {  // round to nearest tf32 (ties away)
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
 }
 
 // UMMA shared-memory descriptor, K-major SWIZZLE_128B: start >> 4, LBO 1 (unused when
@@ -246,11 +261,27 @@ __global__ void __launch_bounds__(192, 1)
     float* tile = reinterpret_cast<float*>(smem) + (warp - 2) * 32 * 33;
     const long long plane = static_cast<long long>(a.OH) * a.owp;
     const long long base = static_cast<long long>(b) * a.M * plane + static_cast<long long>(oy) * a.owp;
+    using T = typename K::T;
+    T* nh = static_cast<T*>(a.out_nhwc);
+    const long long nh_row = (static_cast<long long>(b) * a.OH + oy) * a.OW;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 32) {
       if (ox0 + c0 >= a.OW) break;  // warp-uniform
       uint32_t v[32];
       tmem_ld32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c0, v);
+      if (nh) {  // lane = channel: 32 consecutive channels of one pixel per store instruction
+        if (mrow < a.M) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const int px = ox0 + c0 + j;
+            if (px < a.OW) {
+              const float y = __fadd_rn(__uint_as_float(v[j]), bias);
+              nh[(nh_row + px) * a.nhwc_c + mrow] = to_tc<T>(y > 0.0f ? y : 0.0f);
+            }
+          }
+        }
+        if (!a.out && !a.out_relu) continue;
+      }
 #pragma unroll
       for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = __fadd_rn(__uint_as_float(v[j]), bias);
       __syncwarp();
@@ -344,19 +375,6 @@ void launch_tc(const void* x_nhwc, const void* w_tc, const TcShape& sh, TcArgs a
 }
 
 // ---- layout conversions ---------------------------------------------------------------------
-template <typename T>
-__device__ __forceinline__ T to_tc(float x);
-template <>
-__device__ __forceinline__ __nv_bfloat16 to_tc<__nv_bfloat16>(float x) {
-  return __float2bfloat16_rn(x);
-}
-template <>
-__device__ __forceinline__ float to_tc<float>(float x) {  // round to nearest tf32 (ties away)
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(r) : "f"(x));
-  return __uint_as_float(r);
-}
-
 // CHW (f32 or widened-f32 f64, row pitch wp) -> NHWC T, through a 32x32 smem transpose of
 // (channel, pixel) per image row.
 template <typename S, typename T>
@@ -443,7 +461,7 @@ template void chw_to_nhwc<float>(int, const float*, int, int, int, int, int, voi
 template void chw_to_nhwc<double>(int, const double*, int, int, int, int, int, void*, cudaStream_t);
 
 void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, const TcShape& sh,
-             void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st) {
+             void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st, void* out_nhwc) {
   if (!conv_tc_eligible(kind, sh)) throw_arg("conv_tc: shape not eligible for the tensor-core path");
   TcArgs a;
   std::memset(&a, 0, sizeof a);
@@ -459,6 +477,8 @@ void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, 
   a.owp = sh.out_wp ? sh.out_wp : sh.OW;
   a.relu = relu ? 1 : 0;
   a.out_f64 = out_f64 ? 1 : 0;
+  a.out_nhwc = out_nhwc;
+  a.nhwc_c = tc_padded_c(kind, sh.M);
   if (kind == TC_BF16)
     launch_tc<TC_BF16, 256, 4>(x_nhwc, w_tc, sh, a, st);
   else

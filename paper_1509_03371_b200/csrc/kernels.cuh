@@ -67,9 +67,12 @@ void weights_to_tc(int kind, const float* w, int M, int C, int k, void* out, cud
 template <typename S>
 void chw_to_nhwc(int kind, const S* in, int B, int C, int H, int W, int wp, void* out, cudaStream_t st);
 // out (f32, or f64 widened f32 when out_f64) = conv + bias (relu'd when relu); out_relu
-// (f64 only, nullable) = relu(conv + bias). CHW per image, row pitch sh.out_wp.
+// (f64 only, nullable) = relu(conv + bias). CHW per image, row pitch sh.out_wp. out_nhwc
+// (nullable): relu(conv + bias) written directly as the next tensor-core conv's operand,
+// [B][OH][OW][tc_padded_c(kind, M)] (the padding channels are left untouched: zero them once).
 void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, const TcShape& sh,
-             void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st);
+             void* out, void* out_relu, bool out_f64, bool relu, cudaStream_t st,
+             void* out_nhwc = nullptr);
 
 // ---- train.cu: the backward layer functions and sgd_step (bit-identical, S = float) --------
 // Data blobs: widened-f32 f64, row pitch wp; diffs: compact f32 [C][H][W] of one image.
