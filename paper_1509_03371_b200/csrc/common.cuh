@@ -109,6 +109,10 @@ struct DevBuf {
   T* as() const { return static_cast<T*>(p); }
 };
 
+// Raises a kernel's dynamic shared memory limit to `bytes`, once per (kernel, device): function
+// attributes are per device, and several host threads may drive different devices.
+void ensure_dynamic_smem(const void* func, size_t bytes);
+
 // ConvGeometry::out_extent (tensor.hpp:26-42), messages verbatim.
 int out_extent(int in, int k, int d, int s, int p, const char* what);
 
