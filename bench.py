@@ -399,10 +399,12 @@ def run_ours(args):
         with open(tp) as f:
             tj = json.load(f)
         traffic = tj.get("traffic_bytes_per_launch")
-        traffic_note = (f"dram read+write of one ip1 launch (ncu --set full); algorithmic "
-                        f"{tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.2f} GB: f64 weights "
-                        "re-streamed per CTA wave and dilated input rows re-read from DRAM (L2 hit "
-                        "82.6%) -- 3% of HBM bandwidth, the kernel is DMMA-bound (91.7% pipe active)")
+        traffic_note = (f"dram read+write of one ip1 launch (ncu --set full, profiles/"
+                        f"r01_ip1_ncu_full.json); algorithmic "
+                        f"{tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.2f} GB (f32 weights, "
+                        "input, output): the rest is the f64 input re-read once per f_out block "
+                        "pass (L2 hit 93.6%), ~1% of HBM bandwidth; the kernel is bound by the "
+                        "FP64 tensor pipe (90% active)")
     roofline = {
         "bound": "tensor",
         "pipe": "fp64 tensor (DMMA.8x8x4)",
