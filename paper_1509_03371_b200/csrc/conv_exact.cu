@@ -32,9 +32,12 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace graft {
 namespace {
+
+using namespace ptx;
 
 constexpr int KPAD = 32;     // weight taps padded to this (largest BK)
 constexpr int MPAD = 128;    // weight rows padded to this (largest BM)
@@ -69,32 +72,6 @@ inline void magic_div(int d, unsigned long long* m, int* sh) {
 
 __device__ __forceinline__ int fast_div(int n, unsigned long long m, int sh) {
   return static_cast<int>((static_cast<unsigned long long>(n) * m) >> sh);
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-
-__device__ __forceinline__ void cp_async8_zfill(void* smem, const void* gmem, bool valid) {
-  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  const int sz = valid ? 8 : 0;
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
-}
-
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
-
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-// D = A(8x4, row) * B(4x8, col) + D in fp64; lane l holds A[l/4][l%4], B[l%4][l/4],
-// D[l/4][2*(l%4)+{0,1}]. Sequential fma order k0..k3 (see header comment).
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
 }
 
 // BM x BN block tile, BK taps per chunk, WM x WN warps (WM*WN == 8), STAGES-deep cp.async
@@ -248,31 +225,6 @@ __global__ void __launch_bounds__(NTHREADS, MINB) conv_exact_kernel(const ConvAr
 // only wait on the stage's "full" mbarrier, run LDS + DMMA, and release the stage through its
 // "empty" mbarrier. No CTA-wide barrier in the main loop, so consumers drift freely within
 // the STAGES-deep ring and the DMMA pipe sees no gather/barrier bubbles.
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_cp_async_arrive(uint64_t* bar) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  const unsigned a = static_cast<unsigned>(__cvta_generic_to_shared(bar));
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int NPROD, int MINB>
 __global__ void __launch_bounds__(32 * (WM * WN + NPROD), MINB) conv_ws_kernel(const ConvArgs a) {
   constexpr int NCW = WM * WN;  // consumer warps

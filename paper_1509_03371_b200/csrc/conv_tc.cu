@@ -26,9 +26,12 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace graft {
 namespace {
+
+using namespace ptx;
 
 template <int KIND>
 struct TcKind;
@@ -59,44 +62,6 @@ struct TcArgs {
   void* out_nhwc;      // optional: relu(conv) as the NEXT tc conv's operand, [B][OH][OW][nhwc_c]
   int nhwc_c;          // channel stride of out_nhwc (f_out padded to the K block)
 };
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int x, int y, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%2, %3}], [%4];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* tm, int x, int y, int z, int w,
-                                       uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
-      "{%2, %3, %4, %5}], [%6];\n" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(tm)), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
-      : "memory");
-}
 
 template <typename T>
 __device__ __forceinline__ T to_tc(float x);
@@ -220,8 +185,8 @@ __global__ void __launch_bounds__(192, 1)
         const int s = kb % STAGES;
         if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
         mbar_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_2d(sA + s * A_BYTES, &tmA, tap * a.C + cc * K::BK, m0, &full[s]);
-        tma_4d(sB + s * B_BYTES, &tmB, cc * K::BK, ox0 + kx * a.d, oy + ky * a.d, b, &full[s]);
+        tma_load_2d(sA + s * A_BYTES, &tmA, tap * a.C + cc * K::BK, m0, &full[s]);
+        tma_load_4d(sB + s * B_BYTES, &tmB, cc * K::BK, ox0 + kx * a.d, oy + ky * a.d, b, &full[s]);
         if (++cc == a.cchunks) {
           cc = 0;
           ++tap;

@@ -21,9 +21,12 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "ptx.cuh"
 
 namespace graft {
 namespace {
+
+using namespace ptx;
 
 #define GS_LOOP(i, n)                                                                   \
   for (long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;     \
@@ -31,12 +34,6 @@ namespace {
 
 unsigned grid_for(long long n, int threads = 256) {
   return static_cast<unsigned>(std::max<long long>(1, std::min<long long>((n + threads - 1) / threads, 148LL * 32)));
-}
-
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(d0), "+d"(d1)
-      : "d"(a), "d"(b));
 }
 
 // ---- gemm (inc/tensor.hpp:151-169) on the FP64 tensor pipe ---------------------------------
@@ -184,18 +181,6 @@ void launch_gemm(int m, int n, int k, const TA* a, long long sai, long long sak,
 // and the problem fills the GPU. Operands are copied straight into DMMA fragment order with
 // cp.async (16 bytes = two consecutive k when k is the contiguous index, else 8 bytes), so
 // the next STAGES-1 chunks are in flight while one is multiplied.
-__device__ __forceinline__ void cpa16(double* dst, const double* src, bool v) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(v ? 16 : 0));
-}
-__device__ __forceinline__ void cpa8(double* dst, const double* src, bool v) {
-  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(v ? 8 : 0));
-}
-__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 constexpr int PB = 128, PK = 16, PSTAGES = 4;
 // Operand staging modes: 0 = the m/n index is contiguous (8-byte copies), 1 = k contiguous
 // (8-byte), 2 = k contiguous with 16-byte-aligned rows (16-byte copies of k pairs).
@@ -210,11 +195,11 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
       const int kk = k0 + 2 * kp, row = r0 + rl;
       double* d = dst + ((kp >> 1) * (PB / 8) + (rl >> 3)) * 32 + (rl & 7) * 4 + ((2 * kp) & 3);
       if (row < rmax && kk + 1 < k) {
-        cpa16(d, src + static_cast<long long>(row) * ld + kk, true);
+        cp_async16_zfill(d, src + static_cast<long long>(row) * ld + kk, true);
       } else {  // k tail (or rows past the edge): element-wise, zero-filled
         const bool v0 = row < rmax && kk < k;
-        cpa8(d, v0 ? src + static_cast<long long>(row) * ld + kk : src, v0);
-        cpa8(d + 1, src, false);
+        cp_async8_zfill(d, v0 ? src + static_cast<long long>(row) * ld + kk : src, v0);
+        cp_async8_zfill(d + 1, src, false);
       }
     }
   } else if (MODE == 1) {
@@ -224,7 +209,7 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
       const int kl = q & 15, rl = q >> 4;
       const int kk = k0 + kl, row = r0 + rl;
       const bool v = row < rmax && kk < k;
-      cpa8(dst + ((kl >> 2) * (PB / 8) + (rl >> 3)) * 32 + (rl & 7) * 4 + (kl & 3),
+      cp_async8_zfill(dst + ((kl >> 2) * (PB / 8) + (rl >> 3)) * 32 + (rl & 7) * 4 + (kl & 3),
            v ? src + static_cast<long long>(row) * ld + kk : src, v);
     }
   } else {
@@ -234,7 +219,7 @@ __device__ __forceinline__ void stage_operand(double* dst, const double* __restr
       const int rl = q & 127, kl = q >> 7;
       const int kk = k0 + kl, row = r0 + rl;
       const bool v = row < rmax && kk < k;
-      cpa8(dst + ((kl >> 2) * (PB / 8) + (rl >> 3)) * 32 + (rl & 7) * 4 + (kl & 3),
+      cp_async8_zfill(dst + ((kl >> 2) * (PB / 8) + (rl >> 3)) * 32 + (rl & 7) * 4 + (kl & 3),
            v ? src + static_cast<long long>(kk) * ld + row : src, v);
     }
   }
@@ -265,13 +250,13 @@ __global__ void __launch_bounds__(256, 1) gemm_pipe_kernel(int m, int n, int k, 
 #pragma unroll
   for (int st = 0; st < PSTAGES - 1; ++st) {
     if (st < nch) load(st, st);
-    cpa_commit();
+    cp_async_commit();
   }
   for (int ch = 0; ch < nch; ++ch) {
-    cpa_wait<PSTAGES - 2>();
+    cp_async_wait<PSTAGES - 2>();
     __syncthreads();
     if (ch + PSTAGES - 1 < nch) load(ch + PSTAGES - 1, (ch + PSTAGES - 1) % PSTAGES);
-    cpa_commit();
+    cp_async_commit();
     const double* as = As + (ch % PSTAGES) * PK * PB;
     const double* bs = Bs + (ch % PSTAGES) * PK * PB;
 #pragma unroll
@@ -287,7 +272,7 @@ __global__ void __launch_bounds__(256, 1) gemm_pipe_kernel(int m, int n, int k, 
       }
     }
   }
-  cpa_wait<0>();
+  cp_async_wait<0>();
 #pragma unroll
   for (int x = 0; x < 8; ++x) {
     const int i = i0 + (wm * 8 + x) * 8 + (lane >> 2);
