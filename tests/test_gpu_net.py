@@ -268,3 +268,25 @@ def test_process_single_tile_u_nets(cfg):
         assert dmax <= tol[(cfg, kind)], (cfg, kind, dmax)
         flips = lab_t != res.labels.view()
         assert np.all(np.abs(probs[1] - probs[0])[flips] <= 2 * dmax), "a label flipped away from a near-tie"
+
+
+def test_process_large_ragged_image_properties():
+    """A 2048 x 1536 image through full sk.net (3.1 M labels): the internal 1024-px retiling, the
+    caller's 128-px tiling (the reference's CLI default) and a batch of one give identical
+    planes; labels are the first-maximal class of the probabilities; probabilities sum to 1."""
+    spec = g.parse_netspec_or_throw(config_text("sk.net"))
+    states = g.init_weights(spec, 1)
+    img = g.Rng(4242).index_array_u8(2048 * 1536, 256).reshape(2048, 1536)
+    auto = g.Processor(spec, states)
+    lab, pr = auto.run(img, 128, 101)
+    assert auto.last_tile() > 128
+    plain = g.Processor(spec, states, retile=0)
+    lab2, pr2 = plain.run(img, 128, 101)
+    assert plain.last_tile() == 128
+    assert np.array_equal(lab, lab2)
+    assert_bitwise(pr, pr2, "retiled vs 128-px tiles")
+    labb, prb = auto.run_batch(img[None], 128, 101)
+    assert np.array_equal(labb[0], lab)
+    assert_bitwise(prb[0], pr, "batch of one")
+    assert np.array_equal(lab, (pr[1] > pr[0]).astype(np.uint8))
+    assert np.abs(pr.astype(np.float64).sum(0) - 1.0).max() < 1e-6
