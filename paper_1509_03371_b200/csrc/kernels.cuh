@@ -76,20 +76,20 @@ void conv_tc(int kind, const void* x_nhwc, const void* w_tc, const float* bias, 
 
 // ---- train.cu: the backward layer functions and sgd_step (bit-identical, S = float) --------
 // Data blobs: widened-f32 f64, row pitch wp; diffs: compact f32 [C][H][W] of one image.
-// gemm (tensor.hpp:151-169) on DMMA: C(i,j) = float(alpha*chain + beta*C), strided A and B.
-void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long long sak,
-                      const double* b, long long sbk, long long sbj, double alpha, double beta,
-                      float* c, cudaStream_t st);
-void gemm_dmma_f32out(int m, int n, int k, const float* a, long long sai, long long sak,
-                      const float* b, long long sbk, long long sbj, double alpha, double beta,
-                      float* c, cudaStream_t st);
-// f64-operand variant: 4-stage cp.async DMMA GEMM for problems that fill the GPU, else the
-// shape-adaptive kernel. a_k_contig: A(i,kk) = a[i*lda + kk], else a[kk*lda + i]; likewise B
+// gemm (tensor.hpp:151-169) on DMMA: C(i,j) = float(alpha*chain + beta*C), f64 operands
+// (float values), 4-stage cp.async pipeline, CTA tile chosen by shape. a_k_contig: A(i,kk) = a[i*lda + kk], else a[kk*lda + i]; likewise B
 // with B(kk,j) = b[j*ldb + kk] (k contiguous) or b[kk*ldb + j].
 void gemm_dmma_f64ops(int m, int n, int k, const double* a, bool a_k_contig, long long lda,
                       const double* b, bool b_k_contig, long long ldb, double alpha, double beta,
                       float* c, cudaStream_t st);
 void widen_f32(const float* in, long long n, double* out, cudaStream_t st);
+void transpose_f32(const float* in, int rows, int cols, float* out, cudaStream_t st);
+struct DevBuf;
+// conv_sk_backward's W^T * dOut (gemm TN) on the forward conv kernel as a 1x1 convolution;
+// dy64 = dOut widened, compact [f_out][OH*OW]; col_grad f32 [fan_in][OH*OW]. Scratch buffers
+// (transposed / tiled weights, zero bias) are grown as needed.
+void col_grad_conv(const double* dy64, int f_out, int OH, int OW, const float* w_f32, int fan_in,
+                   DevBuf& wt_f32, DevBuf& wt_tiled, DevBuf& zero_bias, float* col_grad, cudaStream_t st);
 void im2col_pitched(const double* in, int C, int H, int W, int wp, int k, int d, int s, int p,
                     int OH, int OW, double* col, cudaStream_t st);
 void bias_grad(const float* dout, int M, int n, float* bdiff, cudaStream_t st);

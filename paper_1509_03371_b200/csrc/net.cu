@@ -95,7 +95,8 @@ struct graft_net {
   int tile_batch = 0;
   bool keep_blobs = false;
   bool training = false;  // forward records pool argmax (LayerState::argmax) for backward
-  DevBuf col, col_grad, loss_terms, loss_dev, dy64, w64;  // backward / softmax_loss scratch
+  DevBuf col, col_grad, loss_terms, loss_dev, dy64;  // backward / softmax_loss scratch
+  DevBuf wt32, wt_tiled, zero_bias;                  // W^T operands of the col_grad conv
   int retile_cap = 1024;  // largest internal process() tile (0: use the caller's tile)
   int last_tile = 0;      // internal tile used by the last process call
   int tc_kind = 0;        // tolerance mode: 0 = exact (default), TC_BF16 / TC_TF32 = eligible
@@ -958,13 +959,10 @@ void backward_impl(graft_net& n) {
                            true, npx, 1.0, 1.0, l.w_diff.as<float>(), n.stream);
           bias_grad(dout, l.f_out, npx, l.b_diff.as<float>(), n.stream);
           if (l.inputs[0] != "data") {
-            const size_t nw = static_cast<size_t>(l.f_out) * fan_in;
-            n.w64.ensure(std::max<size_t>(nw, 1) * sizeof(double));
-            widen_f32(l.w_f32.as<float>(), static_cast<long long>(nw), n.w64.as<double>(), n.stream);
             n.col_grad.ensure(std::max<size_t>(static_cast<size_t>(fan_in) * npx, 1) * sizeof(float));
-            // col_grad = W^T * dOut: A(i=r, kk=f) = W[f][r], B(kk=f, j=p) = dy[f][p]
-            gemm_dmma_f64ops(fan_in, npx, l.f_out, n.w64.as<double>(), false, fan_in,
-                             n.dy64.as<double>(), false, npx, 1.0, 0.0, n.col_grad.as<float>(), n.stream);
+            // col_grad = W^T * dOut as a 1x1 conv of dOut on the TMA-fed DMMA conv kernel
+            col_grad_conv(n.dy64.as<double>(), l.f_out, OH, OW, l.w_f32.as<float>(), fan_in, n.wt32,
+                          n.wt_tiled, n.zero_bias, n.col_grad.as<float>(), n.stream);
             col2im_add(n.col_grad.as<float>(), in.C, in.H, in.W, l.k, l.d, l.s, l.p, OH, OW, din,
                        n.stream);
           }

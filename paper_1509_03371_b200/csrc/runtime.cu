@@ -567,11 +567,9 @@ int graft_conv_sk_backward_f32(const float* in, int C, int H, int W, const float
                      1.0, 1.0, dw.dev, st);
     bias_grad(dy.dev, f_out, static_cast<int>(npx), db.dev, st);
     if (din) {
-      DevBuf ww = widen(w.dev, nw, st);
-      DevBuf cg(std::max<size_t>(fan_in * npx, 1) * sizeof(float));
-      gemm_dmma_f64ops(static_cast<int>(fan_in), static_cast<int>(npx), f_out, ww.as<double>(), false,
-                       static_cast<long long>(fan_in), dyw.as<double>(), false,
-                       static_cast<long long>(npx), 1.0, 0.0, cg.as<float>(), st);
+      DevBuf cg(std::max<size_t>(fan_in * npx, 1) * sizeof(float)), wt32, wtt, zb;
+      col_grad_conv(dyw.as<double>(), f_out, OH, OW, w.dev, static_cast<int>(fan_in), wt32, wtt, zb,
+                    cg.as<float>(), st);
       col2im_add(cg.as<float>(), C, H, W, k, d, s, p, OH, OW, dx.dev, st);
     }
     dw.finish(st);
