@@ -41,6 +41,7 @@ PARAM_MOMENTUM = 2
 
 TC_BF16 = 1
 TC_TF32 = 2
+TC_BF16X3 = 3
 
 
 class CudaError(Error):

@@ -47,7 +47,7 @@ void conv_f64_muladd(const double* in, const double* w, const double* bias, cons
 // ---- conv_tc.cu (tolerance mode, opt-in) ---------------------------------------------------
 // tcgen05 implicit-GEMM conv: bf16 (kind::f16) or tf32 (kind::tf32) operands, f32 accumulation
 // in TMEM. NOT bit-exact; see conv_tc.cu and DESIGN.md "Tolerance mode".
-enum { TC_BF16 = 1, TC_TF32 = 2 };
+enum { TC_BF16 = 1, TC_TF32 = 2, TC_BF16X3 = 3 };
 struct TcShape {
   int B = 1, C = 0, H = 0, W = 0;  // input, NHWC per image
   int M = 0, k = 1, d = 1, s = 1, p = 0;
@@ -56,6 +56,7 @@ struct TcShape {
 };
 int tc_block_k(int kind);
 size_t tc_elem_bytes(int kind);
+int tc_planes(int kind);  // 2 for the split kinds (hi plane, then lo plane), else 1
 // Operand layouts pad channels to the 128-byte K block and f_out to the 128-row MMA tile
 // with zeros: [Mp][k][k][Cp] weights, [B][H][W][Cp] activations.
 int tc_padded_c(int kind, int C);

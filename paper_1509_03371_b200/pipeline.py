@@ -72,7 +72,7 @@ class Processor:
         caller's w). Every tiling gives bit-identical planes.
 
         tensor_cores: None (default) = the exact fp64 path, bit-identical to the reference;
-        "bf16" / "tf32" = TOLERANCE MODE: eligible convs run on the tcgen05 tensor cores and the
+        "bf16" / "tf32" / "bf16x3" (split bf16, ~fp32 operands) = TOLERANCE MODE: eligible convs run on the tcgen05 tensor cores and the
         planes are only within the tolerance DESIGN.md states (labels may differ on near-ties)."""
         self.spec = spec
         self.states = states
@@ -83,9 +83,10 @@ class Processor:
         if retile is not None:
             self.net.set_option(_lib.OPT_RETILE, retile)
         if tensor_cores is not None:
-            kinds = {"bf16": _lib.TC_BF16, "tf32": _lib.TC_TF32}
+            kinds = {"bf16": _lib.TC_BF16, "tf32": _lib.TC_TF32, "bf16x3": _lib.TC_BF16X3}
             if tensor_cores not in kinds:
-                raise ValueError(f"tensor_cores must be None, 'bf16' or 'tf32', not {tensor_cores!r}")
+                raise ValueError(f"tensor_cores must be None, 'bf16', 'tf32' or 'bf16x3', "
+                                 f"not {tensor_cores!r}")
             self.net.set_option(_lib.OPT_TC_KIND, kinds[tensor_cores])
         self.n_classes = compute_channels(spec)[spec.layers[-1].output]
 

@@ -48,7 +48,7 @@ CASES = [  # B, C, H, W, M, k, d
 ]
 
 
-@pytest.mark.parametrize("kind", [_lib.TC_BF16, _lib.TC_TF32])
+@pytest.mark.parametrize("kind", [_lib.TC_BF16, _lib.TC_TF32, _lib.TC_BF16X3])
 @pytest.mark.parametrize("case", CASES)
 def test_conv_tc_matches_fp64_conv_of_rounded_operands(kind, case):
     B, C, H, W, M, k, d = case
@@ -58,16 +58,20 @@ def test_conv_tc_matches_fp64_conv_of_rounded_operands(kind, case):
     bias = torch.randn(M, device="cuda", generator=gen) * 0.01
     for relu in (False, True):
         got = run_tc(kind, x, w, bias, k, d, relu)
+        tol = TOL
         if kind == _lib.TC_BF16:
             xr, wr = x.bfloat16().double(), w.bfloat16().double()
-        else:
+        elif kind == _lib.TC_TF32:
             xr, wr = round_tf32(x).double(), round_tf32(w).double()
+        else:  # split bf16: against the unrounded operands, operand error ~3 * 2^-17
+            xr, wr = x.double(), w.double()
+            tol = 6e-5
         ref = torch.nn.functional.conv2d(xr, wr, bias.double(), dilation=d)
         if relu:
             ref = ref.clamp_min(0)
         absum = torch.nn.functional.conv2d(xr.abs(), wr.abs(), None, dilation=d)
         err = (got.double() - ref).abs()
-        bound = TOL * absum + ref.abs() * 2.0 ** -23 + 1e-30
+        bound = tol * absum + ref.abs() * 2.0 ** -23 + 1e-30
         worst = (err / bound).max().item()
         assert worst <= 1.0, f"kind {kind} case {case} relu {relu}: err/bound {worst:.3g}"
 
@@ -92,7 +96,7 @@ def test_process_tolerance_mode_full_sk_net():
     states = g.init_weights(spec, 1)
     img = g.Rng(55).index_array_u8(256 * 256, 256).reshape(256, 256)
     lab_x, prob_x = g.Processor(spec, states).run(img, 128, 101)
-    for kind in ("bf16", "tf32"):
+    for kind in ("bf16", "tf32", "bf16x3"):
         proc = g.Processor(spec, states, tensor_cores=kind)
         lab_t, prob_t = proc.run(img, 128, 101)
         dp = np.abs(prob_t - prob_x)

@@ -20,7 +20,7 @@ b = torch.zeros(M, device="cuda")
 OH, OW = H - (k - 1) * d, W - (k - 1) * d
 out = torch.empty(B, M, OH, OW, device="cuda")
 flops = 2.0 * M * C * k * k * OH * OW * B
-for kind, name in ((_lib.TC_BF16, "bf16"), (_lib.TC_TF32, "tf32")):
+for kind, name in ((_lib.TC_BF16, "bf16"), (_lib.TC_TF32, "tf32"), (_lib.TC_BF16X3, "bf16x3")):
     best = 1e9
     for it in range(4):
         torch.cuda.synchronize()

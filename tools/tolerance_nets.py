@@ -9,7 +9,7 @@ for cfg in ("sk.net", "u.net", "usk.net"):
     side = 2 * w if cfg != "sk.net" else 512
     img = g.Rng(9).index_array_u8(side * side, 256).reshape(side, side)
     lab, pr = g.Processor(spec, states).run(img, w, v)
-    for kind in ("bf16", "tf32"):
+    for kind in ("bf16", "tf32", "bf16x3"):
         lt, pt = g.Processor(spec, states, tensor_cores=kind).run(img, w, v)
         d = np.abs(pt - pr); flips = lt != lab
         m = np.abs(pr[1] - pr[0])
