@@ -297,7 +297,9 @@ def run_ours(args):
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         step_device()
-        e1.record(stream)
+        # after the combine: the NCCL gather runs on torch's stream (process() itself ends
+        # with its own stream synchronised), so the step's end is recorded there
+        e1.record(torch.cuda.current_stream())
         e1.synchronize()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)

@@ -67,6 +67,9 @@ bool conv_tc_eligible(int kind, const TcShape& sh);
 void weights_to_tc(int kind, const float* w, int M, int C, int k, void* out, cudaStream_t st);
 template <typename S>
 void chw_to_nhwc(int kind, const S* in, int B, int C, int H, int W, int wp, void* out, cudaStream_t st);
+// maxpool_sk_forward on the tensor-core operand layout (in/out [planes][B][H][W][Cp]).
+void maxpool_tc(int kind, const void* in, int B, int C, int H, int W, int k, int d, int s, int OH, int OW,
+                void* out, cudaStream_t st);
 // out (f32, or f64 widened f32 when out_f64) = conv + bias (relu'd when relu); out_relu
 // (f64 only, nullable) = relu(conv + bias). CHW per image, row pitch sh.out_wp. out_nhwc
 // (nullable): relu(conv + bias) written directly as the next tensor-core conv's operand,
