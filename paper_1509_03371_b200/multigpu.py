@@ -141,7 +141,7 @@ def gather_shards(lab_shard, prob_shard, n_images: int, rank: int, world: int, g
         return out
 
     lp, pp = padded(lab_shard), padded(prob_shard)
-    if world > 1:
+    if world > 1 or (dist.is_available() and dist.is_initialized()):
         la = [torch.empty_like(lp) for _ in range(world)]
         pa = [torch.empty_like(pp) for _ in range(world)]
         dist.all_gather(la, lp, group=group)
