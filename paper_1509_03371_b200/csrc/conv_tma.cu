@@ -53,7 +53,8 @@ struct TmaArgs {
   int tap_stride;  // doubles between tap boxes in smem (multiple of 16)
   int box_bytes;
   int tiles_x, tiles_y;
-  unsigned mblocks;
+  unsigned mblocks;  // f_out blocks of this launch
+  int mb0;           // first f_out block of this launch (a launch may cover a row range)
   int order;         // grid raster: 0 = f_out blocks fastest; 1 = f_out blocks slowest;
                      // 2 = groups of `mgroup` f_out blocks, rows in residue-mod-d order
   int mgroup;
@@ -125,6 +126,7 @@ __global__ void __launch_bounds__(32 * (WM * WN + 1), MINB)
     ty = static_cast<int>(rest % a.tiles_y);
     img = static_cast<int>(rest / a.tiles_y);
   }
+  mb += a.mb0;
   const int ox0 = tx * a.CW, oy0 = ty * a.R;
   const int nchunks = (a.K + BK - 1) / BK;
 
@@ -262,12 +264,15 @@ void magic(int d, unsigned long long* m, int* sh) {
 }
 
 template <int BM, int BN, int BK, int WM, int WN, int STAGES, int MINB>
-void launch(const CUtensorMap& tm, TmaArgs a, cudaStream_t st, long long n_tiles) {
+void launch(const CUtensorMap& tm, TmaArgs a, cudaStream_t st, long long n_tiles, int m_begin = 0,
+            int m_end = -1) {
   const size_t smem = static_cast<size_t>(STAGES) * (BK * BM + BK * a.tap_stride) * sizeof(double) +
                       2 * STAGES * sizeof(uint64_t) + STAGES * sizeof(unsigned);
   auto kern = conv_tma_kernel<BM, BN, BK, WM, WN, STAGES, MINB>;
   ensure_dynamic_smem(reinterpret_cast<const void*>(kern), smem);
-  a.mblocks = static_cast<unsigned>((a.M + BM - 1) / BM);
+  if (m_end < 0) m_end = a.M;
+  a.mb0 = m_begin / BM;  // m_begin is a multiple of BM
+  a.mblocks = static_cast<unsigned>((m_end - m_begin + BM - 1) / BM);
   if (a.mgroup < 1 || a.mblocks % static_cast<unsigned>(a.mgroup) != 0) a.mgroup = 1;
   const long long grid = n_tiles * a.mblocks;
   if (grid > 0x7fffffffLL) throw_arg("conv: too many output pixels in one launch");
@@ -368,7 +373,15 @@ void conv_tma(const double* in, const double* w_tiled, const float* bias, const 
         launch<128, 128, 16, 2, 4, 4, 1>(tm, a, st, n_tiles);
       break;
     case 4:  // 64-row blocks (f_out not a multiple of 128)
-      launch<64, 128, 16, 2, 4, 4, 2>(tm, a, st, n_tiles);
+      if (forced < 0 && sh.M > 128 && 3 * stage_bytes(128, 32) + 64 <= 227 * 1024) {
+        // the 128-row kernel for the first floor(M/128)*128 rows, 64-row blocks for the rest
+        // (conv3: f_out 192 = 128 + 64); disjoint output rows, same per-output chain
+        const int m128 = sh.M / 128 * 128;
+        launch<128, 128, 32, 2, 4, 3, 1>(tm, a, st, n_tiles, 0, m128);
+        launch<64, 128, 16, 2, 4, 4, 2>(tm, a, st, n_tiles, m128, sh.M);
+      } else {
+        launch<64, 128, 16, 2, 4, 4, 2>(tm, a, st, n_tiles);
+      }
       break;
     case 5:  // 128 x 128, 8-tap stages, deep ring
       if (11 * stage_bytes(128, 8) + 200 <= 227 * 1024)
