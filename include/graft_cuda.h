@@ -281,6 +281,11 @@ int graft_rng_fill_index_u8(graft_rng* rng, uint8_t* dst, size_t n, uint64_t m);
 int graft_conv_tc_f32(int kind, const float* in, int B, int C, int H, int W, const float* weights,
                       const float* bias, int f_out, int k, int d, float* out, int relu);
 
+/* Exact integer GEMM on the tcgen05 tensor cores (kind::i8): C[M][N] (int32) = A[M][K] . B[N][K]^T,
+ * A int8 (a_signed) or uint8, B uint8, row-major K-contiguous, K % 16 == 0, |C| < 2^31.
+ * Device pointers. The building block of the exact int8-digit conv studied for round 2. */
+int graft_gemm_i8(const void* a, int a_signed, const uint8_t* b, int M, int N, int K, int32_t* c);
+
 /* FP64 tensor-pipe (DMMA) roofline probe: runs the DMMA issue loop for ~`seconds` on the
  * current device and returns the achieved TFLOP/s (the denominator of roofline.frac). */
 int graft_fp64_peak(double seconds, double* tflops);

@@ -120,6 +120,10 @@ void softmax_loss(const double* scores, int C, int H, int W, int wp, const int* 
                   const uint8_t* mask, long long n_count, float* diff, double* terms, double* loss,
                   cudaStream_t st);
 
+// ---- gemm_i8.cu: exact integer GEMM on tcgen05 (kind::i8), C = A . B^T, K-major operands ----
+void gemm_i8(const void* a, bool a_signed, const uint8_t* b, int M, int N, int K, int32_t* c,
+             cudaStream_t st);
+
 // ---- layers.cu ------------------------------------------------------------------------------
 void f32_to_f64(const float* in, double* out, size_t n, cudaStream_t st);
 void f64_to_f32(const double* in, float* out, size_t n, cudaStream_t st);
