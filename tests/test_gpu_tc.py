@@ -113,3 +113,21 @@ def test_tolerance_mode_option_validation():
     spec = g.parse_netspec_or_throw(config_text("sk"))
     with pytest.raises(ValueError):
         g.Processor(spec, g.init_weights(spec, 1), tensor_cores="fp8")
+
+
+def test_tolerance_mode_batch_and_repeat_are_deterministic():
+    """The tensor-core path is deterministic: a batch of images equals the per-image calls, and a
+    repeated call gives the same planes bit for bit (no atomics, fixed MMA order per tile)."""
+    from conftest import config_text
+
+    spec = g.parse_netspec_or_throw(config_text("sk"))
+    states = g.init_weights(spec, 1)
+    proc = g.Processor(spec, states, tensor_cores="bf16")
+    imgs = np.stack([g.Rng(70 + i).index_array_u8(200 * 240, 256).reshape(200, 240) for i in range(3)])
+    labs, probs = proc.run_batch(imgs, 128, 101)
+    for i in range(3):
+        lab, pr = proc.run(imgs[i], 128, 101)
+        assert np.array_equal(lab, labs[i])
+        assert np.array_equal(pr.view(np.uint32), probs[i].view(np.uint32))
+    lab2, pr2 = proc.run(imgs[0], 128, 101)
+    assert np.array_equal(pr2.view(np.uint32), probs[0].view(np.uint32))
