@@ -286,6 +286,16 @@ int graft_conv_tc_f32(int kind, const float* in, int B, int C, int H, int W, con
  * Device pointers. The building block of the exact int8-digit conv studied for round 2. */
 int graft_gemm_i8(const void* a, int a_signed, const uint8_t* b, int M, int N, int K, int32_t* c);
 
+/* EXACT conv_sk_forward (stride 1, no padding) on the int8 tensor cores: the exact integer
+ * sum of fixed-point operands from 14 residue GEMMs (tcgen05 kind::i8) + CRT, a rigorous
+ * interval around the reference's fp64 chain, and that chain itself (DFMA) for every output
+ * the interval cannot certify. Bit-identical to graft_conv_sk_forward_f32 (relu: fused
+ * relu_forward). Device pointers, in: B x C x H x W; K = C*k*k <= 33000. n_fallback
+ * (nullable) receives the number of outputs recomputed by the chain. */
+int graft_conv_crt_f32(const float* in, int B, int C, int H, int W, const float* weights,
+                       const float* bias, int f_out, int k, int d, float* out, int relu,
+                       unsigned long long* n_fallback);
+
 /* FP64 tensor-pipe (DMMA) roofline probe: runs the DMMA issue loop for ~`seconds` on the
  * current device and returns the achieved TFLOP/s (the denominator of roofline.frac). */
 int graft_fp64_peak(double seconds, double* tflops);

@@ -149,6 +149,7 @@ _SIGS = {
     "graft_softmax_loss_layer_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d), _i]),
     "graft_sgd_step_f32": (_i, [_vp, _vp, _vp, _sz, _d, _d, _d, _i]),
     "graft_gemm_i8": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
+    "graft_conv_crt_f32": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i, _vp]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),
 }

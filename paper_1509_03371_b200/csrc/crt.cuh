@@ -1,0 +1,34 @@
+// crt.cuh -- the exact conv on the int8 tensor cores by certification (conv_crt.cu): the
+// host-side state a net keeps per layer (prepared weights) and per device (scratch).
+#pragma once
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace graft {
+
+// Weights prepared once per upload: [15][Mp][k*k][Cp] int8 (14 residue planes + the u8 |w|
+// ceilings), per-row exponents and L1 norms, and the fixed-point widths chosen for K.
+struct CrtWeights {
+  DevBuf planes, ew, w1;
+  int M = 0, C = 0, k = 0, bw = 0, bx = 0;
+  bool valid = false;
+};
+// Per-launch scratch (grown on demand): activation residue planes, patch sums, residue /
+// bound outputs of the GEMMs, and a small misc block (max|x|, fallback count, overflow list).
+struct CrtScratch {
+  DevBuf xres, s1, x1, res, sabs, misc;
+};
+
+int crt_padded_c(int C);
+bool conv_crt_eligible(const ConvShape& sh);
+void crt_prepare_weights(const float* w_f32, int M, int C, int k, CrtWeights& cw, cudaStream_t st);
+size_t crt_scratch_bytes_per_image(const ConvShape& sh);
+// Same contract as conv_exact (bit-identical outputs; out / out_relu nullable), for stride-1,
+// unpadded layers with K = C*k*k <= 33000. w_f32: [M][C][k][k] f32 (reference order).
+void conv_crt(const double* in, const CrtWeights& cw, const float* w_f32, const float* bias, const ConvShape& sh,
+              double* out, double* out_relu, CrtScratch& scr, cudaStream_t st);
+// Outputs recomputed by the exact chain in the last conv_crt on `scr` (synchronises).
+unsigned long long conv_crt_fallbacks(const CrtScratch& scr, cudaStream_t st);
+
+}  // namespace graft
