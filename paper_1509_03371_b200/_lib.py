@@ -37,6 +37,8 @@ OPT_RETILE = 5
 OPT_LAST_TILE = 6
 OPT_TC_KIND = 7
 OPT_TRAINING = 8
+OPT_CRT_MIN_K = 9
+OPT_CRT_FALLBACKS = 10
 PARAM_DIFF = 1
 PARAM_MOMENTUM = 2
 

@@ -104,6 +104,11 @@ class DeviceNet:
     def set_option(self, opt: int, value: int) -> None:
         _lib.check(_lib.lib().graft_net_set_option(self.h, opt, int(value)))
 
+    def get_option(self, opt: int) -> int:
+        v = _lib.C.c_longlong(0)
+        _lib.check(_lib.lib().graft_net_get_option(self.h, opt, _lib.C.byref(v)))
+        return int(v.value)
+
     def sync_params(self, spec: NetSpec, states: NetStates) -> None:
         """Uploads every conv layer whose host weights/bias differ from the last upload."""
         for i, l in enumerate(spec.layers):
