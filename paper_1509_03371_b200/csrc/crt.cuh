@@ -17,7 +17,7 @@ struct CrtWeights {
 // Per-launch scratch (grown on demand): activation residue planes, patch sums, residue /
 // bound outputs of the GEMMs, and a small misc block (max|x|, fallback count, overflow list).
 struct CrtScratch {
-  DevBuf xres, s1, x1, res, sabs, misc, fails, xf;
+  DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff;
 };
 
 int crt_padded_c(int C);
