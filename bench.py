@@ -265,11 +265,14 @@ def run_ours(args):
         proc.run(img_d, w, V, lab_d, prob_d, mem=_lib.MEM_DEVICE)
         combine()
 
-    # measured FP64 (DMMA) peak, sustained, for the roofline denominator
+    # measured tensor-pipe peaks, sustained, for the roofline denominators: int8 (tcgen05
+    # kind::i8, the residue GEMMs of the exact path) and FP64 (DMMA, the chain path)
     import ctypes
 
     pk = ctypes.c_double()
-    _lib.check(_lib.lib().graft_fp64_peak(2.0, ctypes.byref(pk)))
+    _lib.check(_lib.lib().graft_i8_peak(2.0, ctypes.byref(pk)))
+    i8_peak = pk.value
+    _lib.check(_lib.lib().graft_fp64_peak(1.0, ctypes.byref(pk)))
     peak_sustained = pk.value
 
     for _ in range(args.warmup):
@@ -382,7 +385,7 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (ip1's conv_exact launches) ----
+    # ---- roofline of the dominant kernel ----
     names = [l.name for l in spec.layers]
     ip1 = names.index("ip1")
     wi = proc.last_tile()  # internal tile process() chose (bit-identical planes for any tile)
@@ -390,42 +393,68 @@ def run_ours(args):
     n_tiles = ((H + wi - 1) // wi) * ((W + wi - 1) // wi)
     ip1_flops_total = fl["ip1"] * n_tiles * args.steps
     ip1_ms = ms[ip1]
-    achieved = ip1_flops_total / (ip1_ms * 1e-3) / 1e12 if ip1_ms > 0 else None
     conv_ms = sum(ms[i] for i, l in enumerate(spec.layers) if l.kind == g.LayerKind.ConvSK)
     all_ms = sum(ms[i] for i in range(L))
-    # DRAM bytes of the same ip1 launch (1024-px internal tile) from one committed `ncu --set
-    # full` capture (profiles/r01_ip1_ncu_full.json); only valid for that launch shape.
-    traffic = traffic_note = None
-    tp = os.path.join(ROOT, "profiles", "r01_ip1_ncu_full.json")
-    if os.path.exists(tp) and wi == 1024 and n_tiles * args.steps == runs[ip1]:
-        with open(tp) as f:
-            tj = json.load(f)
-        traffic = tj.get("traffic_bytes_per_launch")
-        traffic_note = (f"dram read+write of one ip1 launch (ncu --set full, profiles/"
-                        f"r01_ip1_ncu_full.json); algorithmic "
-                        f"{tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.2f} GB (f32 weights, "
-                        "input, output): the rest is the f64 input re-read once per f_out block "
-                        "pass (L2 hit 93.6%), ~1% of HBM bandwidth; the kernel is bound by the "
-                        "FP64 tensor pipe (90% active)")
-    roofline = {
-        "bound": "tensor",
-        "pipe": "fp64 tensor (DMMA.8x8x4)",
-        "achieved": achieved,
-        "peak": peak_sustained,
-        "peak_source": "measured live in bench.py: graft_fp64_peak (DMMA issue loop, 2 s sustained); "
-                       "MEASURED_PEAKS.json has no FP64 figure",
-        "unit": "TFLOP/s",
-        "frac": achieved / peak_sustained if achieved else None,
-        "traffic": traffic,
-        "traffic_note": traffic_note,
-        "kernel": f"conv_tma_kernel (ip1: M=1024, K=19200, {wi * wi} px per internal tile)",
-        "flops_per_launch": fl["ip1"] * n_tiles * args.steps / max(1, runs[ip1]),
-        "flops_source": "flop_estimate(sk.net, internal tile + 101), convert.hpp:308-322",
-        "avg_launch_ms": ip1_ms / max(1, runs[ip1]),
-        "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
-        "conv_share_of_step": conv_ms / all_ms if all_ms else None,
-        "whole_net_tflops": fl["total"] * n_tiles * args.steps / (total_ms * 1e-3) / 1e12,
-    }
+    cms = (ctypes.c_double * 4)()
+    cl = ctypes.c_longlong()
+    _lib.check(_lib.lib().graft_net_crt_stats(net, cms, ctypes.byref(cl)))
+    if cl.value > 0:
+        # ip1 on the int8 path: crt_gemm_kernel (14 residue GEMMs + the bound GEMM) dominates.
+        # Algorithmic int8 ops = 15 planes x 2*M*N*K with the layer's own K (channel padding
+        # 192 -> 256 is overhead, not counted).
+        gemm_ms = cms[1]
+        ops = 15 * ip1_flops_total
+        achieved = ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
+        traffic = traffic_note = None
+        tp = os.path.join(ROOT, "profiles", "r01_crt_gemm_ncu_full.json")
+        if os.path.exists(tp) and wi == 1024 and n_tiles * args.steps == cl.value:
+            with open(tp) as f:
+                tj = json.load(f)
+            traffic = tj.get("traffic_bytes_per_launch")
+            traffic_note = (f"dram read+write of one crt_gemm_kernel launch (ncu --set full, profiles/"
+                            f"r01_crt_gemm_ncu_full.json); algorithmic {tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.1f} GB "
+                            "(15 weight planes once, 15 activation planes once, residue bytes + bound words out)")
+        roofline = {
+            "bound": "tensor",
+            "pipe": "int8 tensor (tcgen05.mma kind::i8, UTCIMMA)",
+            "achieved": achieved,
+            "peak": i8_peak,
+            "peak_source": "measured live in bench.py: graft_i8_peak (tcgen05 kind::i8 issue loop on every SM, "
+                           "sustained); MEASURED_PEAKS.json has no int8 figure (nominal 4500 dense)",
+            "unit": "TOPS",
+            "frac": achieved / i8_peak if achieved else None,
+            "traffic": traffic,
+            "traffic_note": traffic_note,
+            "kernel": f"crt_gemm_kernel (ip1: M=1024, K=19200 (padded 25600), 15 planes, {wi * wi} px per launch)",
+            "ops_per_launch": ops / cl.value,
+            "ops_source": "15 x flop_estimate(sk.net, internal tile + 101)['ip1'] (convert.hpp:308-322)",
+            "avg_launch_ms": gemm_ms / cl.value,
+            "gemm_share_of_step": gemm_ms / all_ms if all_ms else None,
+            "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
+            "ip1_breakdown_ms_per_step": {"activation_prep": cms[0] / args.steps, "residue_gemms": cms[1] / args.steps,
+                                          "crt_certify": cms[2] / args.steps, "exact_chain_fallback": cms[3] / args.steps},
+            "ip1_chain_fallbacks_per_launch": proc.net.get_option(_lib.OPT_CRT_FALLBACKS),
+            "ip1_outputs_per_launch": 1024 * wi * wi,
+            "fp64_peak_tflops": peak_sustained,
+            "whole_net_fp64_equiv_tflops": fl["total"] * n_tiles * args.steps / (total_ms * 1e-3) / 1e12,
+        }
+    else:
+        achieved = ip1_flops_total / (ip1_ms * 1e-3) / 1e12 if ip1_ms > 0 else None
+        roofline = {
+            "bound": "tensor",
+            "pipe": "fp64 tensor (DMMA.8x8x4)",
+            "achieved": achieved,
+            "peak": peak_sustained,
+            "peak_source": "measured live in bench.py: graft_fp64_peak (DMMA issue loop, sustained); "
+                           "MEASURED_PEAKS.json has no FP64 figure",
+            "unit": "TFLOP/s",
+            "frac": achieved / peak_sustained if achieved else None,
+            "traffic": None,
+            "kernel": f"conv_tma_kernel (ip1: M=1024, K=19200, {wi * wi} px per internal tile)",
+            "avg_launch_ms": ip1_ms / max(1, runs[ip1]),
+            "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
+            "conv_share_of_step": conv_ms / all_ms if all_ms else None,
+        }
     line = {
         "metric": "labels/s",
         "value": value,

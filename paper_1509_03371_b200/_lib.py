@@ -117,6 +117,7 @@ _SIGS = {
     "graft_net_layer_ms": (_i, [_vp, C.POINTER(_d), _i]),
     "graft_net_layer_stats": (_i, [_vp, C.POINTER(_d), C.POINTER(C.c_longlong), _i]),
     "graft_net_reset_stats": (_i, [_vp]),
+    "graft_net_crt_stats": (_i, [_vp, C.POINTER(_d), C.POINTER(C.c_longlong)]),
     "graft_net_stream": (_vp, [_vp]),
     "graft_fp64_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _i]),
@@ -151,6 +152,7 @@ _SIGS = {
     "graft_softmax_loss_layer_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d), _i]),
     "graft_sgd_step_f32": (_i, [_vp, _vp, _vp, _sz, _d, _d, _d, _i]),
     "graft_gemm_i8": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
+    "graft_i8_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_conv_crt_f32": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i, _vp]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),

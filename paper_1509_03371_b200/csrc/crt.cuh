@@ -18,6 +18,14 @@ struct CrtWeights {
 // bound outputs of the GEMMs, and a small misc block (max|x|, fallback count, overflow list).
 struct CrtScratch {
   DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff;
+  // timed mode: device ms accumulated per stage (0 prep, 1 residue GEMMs, 2 certify, 3 chain)
+  cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  double ms[4] = {0, 0, 0, 0};
+  long long gemm_launches = 0;
+  ~CrtScratch() {
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
 };
 
 int crt_padded_c(int C);
@@ -27,7 +35,7 @@ size_t crt_scratch_bytes_per_image(const ConvShape& sh);
 // Same contract as conv_exact (bit-identical outputs; out / out_relu nullable), for stride-1,
 // unpadded layers with K = C*k*k <= 33000. w_f32: [M][C][k][k] f32 (reference order).
 void conv_crt(const double* in, const CrtWeights& cw, const float* w_f32, const float* bias, const ConvShape& sh,
-              double* out, double* out_relu, CrtScratch& scr, cudaStream_t st);
+              double* out, double* out_relu, CrtScratch& scr, cudaStream_t st, bool timed = false);
 // Outputs recomputed by the exact chain in the last conv_crt on `scr` (synchronises).
 unsigned long long conv_crt_fallbacks(const CrtScratch& scr, cudaStream_t st);
 

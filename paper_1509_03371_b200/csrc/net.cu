@@ -330,7 +330,7 @@ int run_layers(graft_net& n, bool mode_process) {
             // exact: int8 residue GEMMs on tcgen05 + CRT + certification + chain fallback
             if (!l.crt.valid) crt_prepare_weights(l.w_f32.as<float>(), l.f_out, in.C, l.k, l.crt, n.stream);
             conv_crt(in.buf.as<double>(), l.crt, l.w_f32.as<float>(), l.bias_dev.as<float>(), sh, out,
-                     out_relu, n.crt_scratch, n.stream);
+                     out_relu, n.crt_scratch, n.stream, n.timed);
           } else {
             conv_exact(in.buf.as<double>(), l.w_tiled.as<double>(), l.bias_dev.as<float>(), sh,
                        out, out_relu, nullptr, n.stream);
@@ -909,6 +909,16 @@ int graft_net_reset_stats(graft_net* n) {
     if (!n) throw_arg("NULL argument");
     n->layer_ms.assign(n->layers.size(), 0.0);
     n->layer_runs.assign(n->layers.size(), 0);
+    for (double& v : n->crt_scratch.ms) v = 0.0;
+    n->crt_scratch.gemm_launches = 0;
+  });
+}
+
+int graft_net_crt_stats(const graft_net* n, double* ms, long long* gemm_launches) {
+  return guard([&] {
+    if (!n || !ms || !gemm_launches) throw_arg("NULL argument");
+    for (int i = 0; i < 4; ++i) ms[i] = n->crt_scratch.ms[i];
+    *gemm_launches = n->crt_scratch.gemm_launches;
   });
 }
 
