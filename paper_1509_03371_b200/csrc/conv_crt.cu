@@ -812,9 +812,18 @@ __global__ void __launch_bounds__(FIN_THREADS, 4)
 // into a two-stage shared-memory ring, one chunk ahead of the DFMA chains. The tail chunk is
 // zero-filled: acc + 0*0 == acc exactly (acc is never -0: it starts at +0 and RN sums of
 // opposite values are +0).
-constexpr int CH_THREADS = 128, CH_SLOTS = 2, CH_TK = 16, CH_WROW = CH_TK + 4;  // 80-byte rows
+#ifndef CRT_CH_THREADS
+#define CRT_CH_THREADS 128
+#define CRT_CH_SLOTS 2
+#define CRT_CH_TK 8
+#endif
+constexpr int CH_THREADS = CRT_CH_THREADS, CH_SLOTS = CRT_CH_SLOTS, CH_TK = CRT_CH_TK,
+              CH_WROW = CH_TK + 4;  // 16-byte-aligned rows, conflict-free LDS.128
 
-__global__ void __launch_bounds__(CH_THREADS)
+#ifndef CRT_CH_MINB
+#define CRT_CH_MINB 8  // 64 registers, 26 KB smem: 32 warps per SM
+#endif
+__global__ void __launch_bounds__(CH_THREADS, CRT_CH_MINB)
     crt_chain_kernel(const CrtFinishArgs a) {
   __shared__ __align__(16) float sW[2][CH_SLOTS][CH_THREADS][CH_WROW];
   __shared__ __align__(16) float sP[2][CH_TK][FIN_PX];

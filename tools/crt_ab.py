@@ -59,6 +59,10 @@ def main():
         per_layer = {spec.layers[i].name: round(ms[i] / args.steps, 2) for i in range(L) if ms[i] > 0.05 * args.steps}
         step = tot / args.steps
         fb = proc.net.get_option(_lib.OPT_CRT_FALLBACKS) if mk else 0
+        cms = (ctypes.c_double * 4)()
+        cl = ctypes.c_longlong()
+        _lib.check(_lib.lib().graft_net_crt_stats(net, cms, ctypes.byref(cl)))
+        crt_ms = [round(x / args.steps, 2) for x in cms]
         results[mk] = (lab.cpu().numpy(), prob.cpu().numpy())
         same = ""
         if len(results) > 1:
@@ -66,7 +70,7 @@ def main():
             same = (f" labels identical {np.array_equal(l0, results[mk][0])}, probs bit-identical "
                     f"{np.array_equal(p0.view(np.uint32), results[mk][1].view(np.uint32))}")
         print(json.dumps({"crt_min_k": mk, "ms_per_step": round(step, 2),
-                          "labels_per_s": round(H * W / (step * 1e-3)), "chain_fallbacks": fb,
+                          "labels_per_s": round(H * W / (step * 1e-3)), "chain_fallbacks": fb, "crt_ms_prep_gemm_certify_chain": crt_ms,
                           "layers_ms": per_layer}) + same,
               flush=True)
         del proc
