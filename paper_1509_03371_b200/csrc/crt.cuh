@@ -17,7 +17,7 @@ struct CrtWeights {
 // Per-launch scratch (grown on demand): activation residue planes, patch sums, residue /
 // bound outputs of the GEMMs, and a small misc block (max|x|, fallback count, overflow list).
 struct CrtScratch {
-  DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff;
+  DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff, approx;
   // timed mode: device ms accumulated per stage (0 prep, 1 residue GEMMs, 2 certify, 3 chain)
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double ms[4] = {0, 0, 0, 0};
