@@ -399,11 +399,16 @@ def run_ours(args):
     cl = ctypes.c_longlong()
     _lib.check(_lib.lib().graft_net_crt_stats(net, cms, ctypes.byref(cl)))
     if cl.value > 0:
-        # ip1 on the int8 path: crt_gemm_kernel (14 residue GEMMs + the bound GEMM) dominates.
-        # Algorithmic int8 ops = 15 planes x 2*M*N*K with the layer's own K (channel padding
-        # 192 -> 256 is overhead, not counted).
+        # ip1 on the int8 path: crt_gemm2_kernel dominates. Algorithmic int8 ops = 2*M*N*K with
+        # the layer's own K times (14 residue planes + the bound plane + the chain-chunk sum
+        # planes, each over 1/nchunk of K: nchunk = C / 64 for C = 192, conv_crt.cu crt_chunk_bytes)
         gemm_ms = cms[1]
-        ops = 15 * ip1_flops_total
+        c_ip1 = 192
+        cq = (c_ip1 + 15) // 16 * 16
+        kb = 64 if cq % 128 else 128
+        nchunk = -(-cq // kb)
+        planes = 15 + (nchunk - 1) / nchunk
+        ops = planes * ip1_flops_total
         achieved = ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
         traffic = traffic_note = None
         tp = os.path.join(ROOT, "profiles", "r01_crt_gemm_ncu_full.json")
@@ -425,9 +430,9 @@ def run_ours(args):
             "frac": achieved / i8_peak if achieved else None,
             "traffic": traffic,
             "traffic_note": traffic_note,
-            "kernel": f"crt_gemm_kernel (ip1: M=1024, K=19200 (padded 25600), 15 planes, {wi * wi} px per launch)",
+            "kernel": f"crt_gemm2_kernel (ip1: M=1024, K=19200, 15 full planes + {nchunk - 1} chunk-sum planes, {wi * wi} px per launch)",
             "ops_per_launch": ops / cl.value,
-            "ops_source": "15 x flop_estimate(sk.net, internal tile + 101)['ip1'] (convert.hpp:308-322)",
+            "ops_source": f"{planes:.3f} planes x flop_estimate(sk.net, internal tile + 101)['ip1'] (convert.hpp:308-322)",
             "avg_launch_ms": gemm_ms / cl.value,
             "gemm_share_of_step": gemm_ms / all_ms if all_ms else None,
             "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
