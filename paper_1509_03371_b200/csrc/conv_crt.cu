@@ -512,7 +512,11 @@ __global__ void __launch_bounds__(192, 1)
       const int buf = i & 1;
       const bool is_mod = tl.plane < NMOD;
       const int p = is_mod ? crt_mod(tl.plane) : 1;
-      const double invp = 1.0 / p;
+      // acc mod p in integer ALU ops: n = acc + off (off a multiple of p above |acc| <= K*128^2
+      // < 2^30, so 0 < n < 2^32), q = floor(n * ceil(2^40/p) / 2^40) is exact for n < 2^32, p <= 256
+      const unsigned up = static_cast<unsigned>(p);
+      const unsigned long long m64 = ((1ull << 40) + up - 1) / up;
+      const unsigned off = up * (((1u << 30) + up - 1) / up);
       mbar_wait(&tfull[buf], static_cast<unsigned>((i >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const long long plane_px = static_cast<long long>(a.OH) * a.OW;
@@ -525,12 +529,9 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < 32; ++j) {
           uint32_t r = v[j];
           if (is_mod) {
-            const int sv = static_cast<int>(v[j]);
-            int qq = static_cast<int>(floor(static_cast<double>(sv) * invp));
-            int rr = sv - qq * p;
-            if (rr < 0) rr += p;
-            if (rr >= p) rr -= p;
-            r = static_cast<uint32_t>(rr);
+            const unsigned n = v[j] + off;
+            const unsigned qq = static_cast<unsigned>((static_cast<unsigned long long>(n) * m64) >> 40);
+            r = n - qq * up;
           }
           tile[lane * 33 + j] = r;
         }
