@@ -537,7 +537,20 @@ __global__ void __launch_bounds__(192, 1)
         }
         __syncwarp();
         const int px = tl.ox0 + c0 + lane;
-        if (px < a.OW) {
+        if (is_mod && (a.OW & 3) == 0 && tl.ox0 + c0 + 32 <= a.OW) {
+          // residue bytes packed 4 pixels per 32-bit store: lane = (row within a group of 4,
+          // 4-pixel group); conflict-free reads of the padded tile
+          const int rsub = lane >> 3, cg = lane & 7;
+          uint8_t* base = a.res + (static_cast<long long>(tl.plane) * a.B + tl.b) * a.Mp * plane_px +
+                          static_cast<long long>(tl.oy) * a.OW + tl.ox0 + c0 + 4 * cg;
+#pragma unroll
+          for (int r4 = 0; r4 < 8; ++r4) {
+            const int rr = 4 * r4 + rsub;
+            const uint32_t* t = tile + rr * 33 + 4 * cg;
+            const uint32_t word = (t[0] & 0xffu) | ((t[1] & 0xffu) << 8) | ((t[2] & 0xffu) << 16) | (t[3] << 24);
+            *reinterpret_cast<uint32_t*>(base + static_cast<long long>(tl.m0 + q * 32 + rr) * plane_px) = word;
+          }
+        } else if (px < a.OW) {
           const long long row0 = static_cast<long long>(tl.oy) * a.OW + px;
           if (is_mod) {
             uint8_t* dst = a.res + (static_cast<long long>(tl.plane) * a.B + tl.b) * a.Mp * plane_px + row0;
