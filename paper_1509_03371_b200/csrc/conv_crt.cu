@@ -473,14 +473,27 @@ __global__ void __launch_bounds__(192, 1)
         const CrtTile tl = crt_tile(a, t, mpairs, BN, rank);
         int dp, s0, s1;
         plane_range(tl.plane, dp, s0, s1);
-        const int nkb = a.k * a.k * ((s1 - s0 + SUB - 1) / SUB);
+        // a single-sub-chunk plane (chunk sums) packs SUB consecutive taps into each stage
+        const bool packed = SUB > 1 && s1 - s0 == 1;
+        const int kk2 = a.k * a.k;
+        const int nkb = packed ? (kk2 + SUB - 1) / SUB : kk2 * ((s1 - s0 + SUB - 1) / SUB);
         int cc = s0, ky = 0, kx = 0, tap = 0;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = static_cast<int>(g % STAGES);
-          const int nsub = min(SUB, s1 - cc);
+          const int nsub = packed ? min(SUB, kk2 - kb * SUB) : min(SUB, s1 - cc);
           if (g >= STAGES) mbar_wait(&empty[s], static_cast<unsigned>(((g / STAGES) - 1) & 1));
           if (leader) mbar_expect_tx(&full[s], 2 * nsub * (A_BYTES + HB_BYTES));
           const uint32_t fb = mapa_rank(&full[s], 0);
+          if (packed) {
+            for (int sc = 0; sc < nsub; ++sc) {
+              const int tp = kb * SUB + sc, pky = tp / a.k, pkx = tp % a.k;
+              tma2_load_2d(sA + (s * SUB + sc) * A_BYTES, &tmA, tp * a.Cp + s0 * KB, dp * a.Mp + tl.m0, fb);
+              tma2_load_4d(sB + (s * SUB + sc) * HB_BYTES, &tmB, s0 * KB,
+                           tl.ox0 + static_cast<int>(rank) * (BN / 2) + pkx * a.d, tl.oy + pky * a.d,
+                           dp * a.B + tl.b, fb);
+            }
+            continue;
+          }
           for (int sc = 0; sc < nsub; ++sc) {
             tma2_load_2d(sA + (s * SUB + sc) * A_BYTES, &tmA, tap * a.Cp + (cc + sc) * KB, dp * a.Mp + tl.m0, fb);
             tma2_load_4d(sB + (s * SUB + sc) * HB_BYTES, &tmB, (cc + sc) * KB,
@@ -508,7 +521,9 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t idesc = tl.plane != BOUND_PLANE ? idesc_crt2<BN>(true) : idesc_crt2<BN>(false);
         int dp, s0, s1;
         plane_range(tl.plane, dp, s0, s1);
-        const int nkb = a.k * a.k * ((s1 - s0 + SUB - 1) / SUB);
+        const bool packed = SUB > 1 && s1 - s0 == 1;
+        const int kk2 = a.k * a.k;
+        const int nkb = packed ? (kk2 + SUB - 1) / SUB : kk2 * ((s1 - s0 + SUB - 1) / SUB);
         const int buf = i & 1;
         if (i >= 2) mbar_wait(&tempty[buf], static_cast<unsigned>(((i >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
@@ -516,7 +531,7 @@ __global__ void __launch_bounds__(192, 1)
         int cc = s0;
         for (int kb = 0; kb < nkb; ++kb, ++g) {
           const int s = static_cast<int>(g % STAGES);
-          const int nsub = min(SUB, s1 - cc);
+          const int nsub = packed ? min(SUB, kk2 - kb * SUB) : min(SUB, s1 - cc);
           mbar_wait(&full[s], static_cast<unsigned>((g / STAGES) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll
@@ -526,15 +541,17 @@ __global__ void __launch_bounds__(192, 1)
                                             : sw64_desc_i8(sA + (s * SUB + sc) * A_BYTES);
               const uint64_t db = KB == 128 ? sw128_desc_i8(sB + (s * SUB + sc) * HB_BYTES)
                                             : sw64_desc_i8(sB + (s * SUB + sc) * HB_BYTES);
-              const int nm = (cc + sc == a.cchunks - 1) ? a.last_mmas : MMAS;
+              const int nm = ((packed ? s0 : cc + sc) == a.cchunks - 1) ? a.last_mmas : MMAS;
 #pragma unroll
               for (int kk = 0; kk < MMAS; ++kk)
                 if (kk < nm) mma2_i8(acc, da + (kk * 32 >> 4), db + (kk * 32 >> 4), idesc, (kb | sc | kk) != 0);
             }
           }
           commit2_mc(&empty[s], static_cast<uint16_t>(0x3));
-          cc += nsub;
-          if (cc == s1) cc = s0;
+          if (!packed) {
+            cc += nsub;
+            if (cc == s1) cc = s0;
+          }
         }
         commit2_mc(&tfull[buf], static_cast<uint16_t>(0x3));
       }
