@@ -7,17 +7,22 @@
 //     launch (|Wi| <= 2^bw, |Xi| <= 2^bx, bw + bx chosen so K * 2^(bw+bx) < Mprod / 2);
 //  2. the exact integer P = sum Wi*Xi is computed modulo 14 pairwise-coprime moduli <= 256 --
 //     each one an s8 x s8 -> s32 implicit-GEMM conv on tcgen05 (kind::i8, exact in any order)
-//     -- and reconstructed by CRT (Ozaki scheme II);
-//  3. a rigorous interval [V - E, V + E] holds the reference's acc: E = fixed-point truncation
-//     (2^-(sw+1) sum|x| + 2^-(sx+1) sum|W~|) + the chain's own rounding bound
-//     u (1 + gamma_K) sum_kk (K - kk) |w x| (recursive summation: step kk's rounding is at most
-//     u |partial sum|), bounded by one more u8 x u8 GEMM on 8-bit ceilings of the position-
-//     weighted |w| (K - kk) / K and of |x|;
+//     -- and reconstructed by CRT (Ozaki scheme II) from three exact 37-bit limb sums;
+//  3. a rigorous interval [V - E, V + E] holds the reference's acc. E = fixed-point truncation
+//     (2^-(sw+1) sum|x| + 2^-(sx+1) sum|W~|) + the chain's own rounding: step kk rounds by at
+//     most u |S_kk| (recursive summation), and with the chain cut into chunks q of L taps
+//     (KB channels x k*k: the GEMM's sub-chunks), sum_kk |S_kk| <= sum_q L |S(start of q)| +
+//     sum_kk (end_q - kk) |w x|. The last sum comes from one u8 x u8 GEMM on 8-bit ceilings of
+//     |w| (end - kk) / L and |x|; the chunk sums from 7-bit s8 x s8 GEMMs over each chunk's
+//     channels, with their quantisation error bounded from per-chunk |x| and |w| sums;
 //  4. when both ends give the same output bits (float(.) + bias, relu if fused), that IS the
-//     reference's output; every other output (about 1% on sk.net's ip1) is recomputed by the
-//     reference's own fp64 chain (DFMA, ascending kk) in the same kernel.
-// Results are bit-identical to conv_exact by construction; tests/test_gpu_crt.py checks it.
-// Feasibility / prototype: tools/crt_prototype.py, profiles/r01_ozaki_feasibility.txt.
+//     reference's output; every other output (0.28% of sk.net's ip1 on the bench image) is
+//     recomputed by the reference's own fp64 chain (DFMA, ascending kk).
+// Kernels: crt_weights (once per upload), crt_xmax / crt_x / crt_xsum (activation prep),
+// crt_gemm2 (all GEMM planes, CTA pairs), crt_certify (CRT + bound + certification), crt_chain
+// (+ crt_overflow) (the fallback chains). Results are bit-identical to conv_exact by
+// construction; tests/test_gpu_crt.py and the full-net goldens check it. Prototype:
+// tools/crt_prototype.py; DESIGN.md "Exact mode on the int8 tensor cores".
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
