@@ -521,6 +521,8 @@ __global__ void __launch_bounds__(192, 1)
     if (leader && lane == 0) {
       long long g = 0;
       int i = 0;
+      const uint64_t da0 = KB == 128 ? sw128_desc_i8(sA) : sw64_desc_i8(sA);
+      const uint64_t db0 = KB == 128 ? sw128_desc_i8(sB) : sw64_desc_i8(sB);
       for (long long t = cid; t < n_pairs; t += ncl, ++i) {
         const CrtTile tl = crt_tile(a, t, mpairs, BN, rank);
         const uint32_t idesc = tl.plane != BOUND_PLANE ? idesc_crt2<BN>(true) : idesc_crt2<BN>(false);
@@ -542,10 +544,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
           for (int sc = 0; sc < SUB; ++sc) {
             if (sc < nsub) {
-              const uint64_t da = KB == 128 ? sw128_desc_i8(sA + (s * SUB + sc) * A_BYTES)
-                                            : sw64_desc_i8(sA + (s * SUB + sc) * A_BYTES);
-              const uint64_t db = KB == 128 ? sw128_desc_i8(sB + (s * SUB + sc) * HB_BYTES)
-                                            : sw64_desc_i8(sB + (s * SUB + sc) * HB_BYTES);
+              // descriptors: the base descriptor plus the slot's byte offset >> 4 (start-address field)
+              const uint64_t da = da0 + static_cast<uint64_t>(((s * SUB + sc) * A_BYTES) >> 4);
+              const uint64_t db = db0 + static_cast<uint64_t>(((s * SUB + sc) * HB_BYTES) >> 4);
               const int nm = ((packed ? s0 : cc + sc) == a.cchunks - 1) ? a.last_mmas : MMAS;
 #pragma unroll
               for (int kk = 0; kk < MMAS; ++kk)
