@@ -329,8 +329,10 @@ int run_layers(graft_net& n, bool mode_process) {
           } else if (n.crt_min_k > 0 && fan_in >= n.crt_min_k && conv_crt_eligible(sh)) {
             // exact: int8 residue GEMMs on tcgen05 + CRT + certification + chain fallback
             if (!l.crt.valid) crt_prepare_weights(l.w_f32.as<float>(), l.f_out, in.C, l.k, l.crt, n.stream);
-            conv_crt(in.buf.as<double>(), l.crt, l.w_f32.as<float>(), l.bias_dev.as<float>(), sh, out,
-                     out_relu, n.crt_scratch, n.stream, n.timed);
+            if (!conv_crt(in.buf.as<double>(), l.crt, l.w_f32.as<float>(), l.bias_dev.as<float>(), sh, out,
+                          out_relu, n.crt_scratch, n.stream, n.timed))
+              conv_exact(in.buf.as<double>(), l.w_tiled.as<double>(), l.bias_dev.as<float>(), sh, out, out_relu,
+                         nullptr, n.stream);
           } else {
             conv_exact(in.buf.as<double>(), l.w_tiled.as<double>(), l.bias_dev.as<float>(), sh,
                        out, out_relu, nullptr, n.stream);
