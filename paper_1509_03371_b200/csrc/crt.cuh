@@ -34,7 +34,8 @@ void crt_prepare_weights(const float* w_f32, int M, int C, int k, CrtWeights& cw
 size_t crt_scratch_bytes_per_image(const ConvShape& sh);
 // Same contract as conv_exact (bit-identical outputs; out / out_relu nullable), for stride-1,
 // unpadded layers with K = C*k*k <= 33000. w_f32: [M][C][k][k] f32 (reference order). Returns
-// false when uncertified outputs overflowed every list (NaN / Inf operands): rerun on conv_exact.
+// false when uncertified outputs overflowed every list (NaN / Inf operands) or the scratch could
+// not be allocated: rerun the layer on conv_exact.
 bool conv_crt(const double* in, const CrtWeights& cw, const float* w_f32, const float* bias, const ConvShape& sh,
               double* out, double* out_relu, CrtScratch& scr, cudaStream_t st, bool timed = false);
 // Outputs recomputed by the exact chain in the last conv_crt on `scr` (synchronises).
