@@ -102,28 +102,38 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ CPU baseline
-def cpu_reference_sample(threads: int, w_out: int, seed_img: int = 55):
-    """The reference's own NetRunner<float>::forward (oracle/_ref) -- or the C restatement when
-    _ref is absent -- on `threads` host threads at once, each over one w_out x w_out tile of
-    process()'s tiling of the workload image. Returns (labels, wall_s, flops, kind)."""
+def cpu_reference_sample(threads: int, w_out: int, size: int = 1024, seed_img: int = 55):
+    """The reference's own NetRunner<float>::forward (oracle/_ref: the unmodified reference
+    headers; the C restatement only when _ref is absent) on `threads` host threads at once, each
+    over one w_out x w_out-label tile of the workload image (the window process() would read for
+    that tile: mirror_pad + normalize_image by the reference's own functions). Nothing from the
+    paper_1509_03371_b200 package is imported on this path. Returns a dict with the sample's
+    labels, wall seconds, and FLOPs by the reference's own flop_estimate (convert.hpp:308-322)."""
     from oracle import oracle as O
 
-    import paper_1509_03371_b200 as g
-
     text = sk_text()
-    spec = g.parse_netspec_or_throw(text)
     w0 = w_out + V
-    img = g.Rng(seed_img).index_array_u8(1024 * 1024, 256).reshape(1024, 1024)
-    padded = O.normalize(O.mirror_pad(img, V))
+    img = O.Rng(seed_img).index_u8(size * size).reshape(size, size)
     kind = "reference" if O.ref_available() else "port"
+    if kind == "reference":
+        R = O.ref()
+        padded_u8 = np.empty((size + V, size + V), np.uint8)
+        assert R.ref_mirror_pad_u8(O.p(img), size, size, V, O.p(padded_u8)) == 0
+        padded = np.empty(padded_u8.shape, np.float32)
+        R.ref_normalize_f32(O.p(padded_u8), padded_u8.size, O.p(padded))
+    else:
+        padded = O.normalize(O.mirror_pad(img, V))
     nets = []
     for t in range(threads):
-        oy, ox = (t * w_out) % (1024 - w_out), ((t * 7 + 3) * w_out) % (1024 - w_out)
+        oy, ox = (t * w_out) % (size - w_out), ((t * 7 + 3) * w_out) % (size - w_out)
         x = np.ascontiguousarray(np.broadcast_to(padded[oy:oy + w0, ox:ox + w0], (3, w0, w0)))
         if kind == "reference":
             nets.append((O.RefNet(text, seed=1), x))
-        else:
-            nets.append((O.init_weights(spec, 1), x))
+        else:  # pragma: no cover - only without oracle/_ref
+            from paper_1509_03371_b200.netspec import parse_netspec_or_throw
+
+            spec = parse_netspec_or_throw(text)
+            nets.append(((spec, O.init_weights(spec, 1)), x))
     errs = []
 
     def work(i):
@@ -132,7 +142,7 @@ def cpu_reference_sample(threads: int, w_out: int, seed_img: int = 55):
             if kind == "reference":
                 net.forward(x)
             else:
-                O.forward_net(spec, net, x)
+                O.forward_net(net[0], net[1], x)
         except Exception as e:  # pragma: no cover
             errs.append(e)
 
@@ -145,47 +155,75 @@ def cpu_reference_sample(threads: int, w_out: int, seed_img: int = 55):
     wall = time.perf_counter() - t0
     if errs:
         raise errs[0]
-    flops = g.flop_estimate(spec, w0)["total"] * threads
-    return threads * w_out * w_out, wall, flops, kind
+    if kind == "reference":
+        flop_tile = O.ref().ref_net_flops(nets[0][0].h, w0)
+        flop_work_tile = O.ref().ref_net_flops(nets[0][0].h, 128 + V)
+    else:  # pragma: no cover
+        from paper_1509_03371_b200.netspec import flop_estimate, parse_netspec_or_throw
+
+        spec = parse_netspec_or_throw(text)
+        flop_tile = flop_estimate(spec, w0)["total"]
+        flop_work_tile = flop_estimate(spec, 128 + V)["total"]
+    return {"labels": threads * w_out * w_out, "wall": wall, "flops": flop_tile * threads,
+            "kind": kind, "flop_per_label_workload": flop_work_tile / (128 * 128)}
 
 
-def cpu_baseline_obj(threads: int, w_out: int):
-    import paper_1509_03371_b200 as g
+def cpu_baseline_obj(threads: int, w_out: int, size: int = 1024):
+    """One bounded sample of the workload on the host, expressed in the workload's unit.
 
-    labels, wall, flops, kind = cpu_reference_sample(threads, w_out)
-    spec = g.parse_netspec_or_throw(sk_text())
-    flop_per_label_workload = g.flop_estimate(spec, 128 + V)["total"] / (128 * 128)
-    measured = labels / wall
-    scaled = (flops / wall) / flop_per_label_workload
+    The reference needs ~10 core-minutes per 128-label tile of the workload, so a step times
+    `threads` concurrent forwards of w_out x w_out-label tiles (input w_out + 101) and converts
+    the measured FLOP rate to labels/s of the workload's tiling with the reference's own
+    flop_estimate: labels_equiv = sample FLOPs / FLOP-per-label at the 128-px tile. The small
+    sample tile favours the CPU (its naive GEMM loop runs faster on the small operands)."""
+    r = cpu_reference_sample(threads, w_out, size)
+    labels_equiv = r["flops"] / r["flop_per_label_workload"]
     return {
-        "value": scaled,
+        "value": labels_equiv / r["wall"],
         "unit": "labels/s",
         "cores": threads,
-        "kind": kind,
-        "sample": (f"{threads} threads x one sk.net forward of a {w_out}x{w_out}-label tile "
-                   f"(input {w_out + V}) of the workload image, concurrently; measured "
-                   f"{measured:.3f} labels/s = {flops / wall / 1e9:.2f} GFLOP/s, scaled to the "
-                   f"workload's 128-tile FLOP/label ({flop_per_label_workload / 1e6:.2f} MFLOP)"),
-        "sample_labels_per_s": measured,
-        "sample_seconds": wall,
+        "kind": r["kind"],
+        "sample": (f"{threads} threads x one reference NetRunner<float>::forward of a {w_out}x{w_out}-label "
+                   f"tile (input {w_out + V}) of the {size}x{size} workload image, concurrently: "
+                   f"{r['labels']} labels, {r['flops'] / 1e9:.2f} GFLOP (reference flop_estimate) in "
+                   f"{r['wall']:.2f} s = {r['flops'] / r['wall'] / 1e9:.2f} GFLOP/s; value = that rate / "
+                   f"{r['flop_per_label_workload'] / 1e6:.3f} MFLOP per label (the workload's 128-px "
+                   f"tiling, reference flop_estimate) = {labels_equiv:.1f} workload labels per sample"),
+        "sample_labels": r["labels"],
+        "sample_labels_per_s": r["labels"] / r["wall"],
+        "sample_gflop": r["flops"] / 1e9,
+        "labels_equiv_per_sample": labels_equiv,
+        "sample_seconds": r["wall"],
     }
 
 
 def run_reference(args):
+    """The reference arm: the reference's own CPU implementation (oracle/_ref) on all host
+    cores; imports nothing from paper_1509_03371_b200 (only oracle/ is loaded)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     threads = args.cpu_threads or os.cpu_count() or 1
     vals = []
-    cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline_obj(threads, args.cpu_tile)
+        cb = cpu_baseline_obj(threads, args.cpu_tile, args.size)
         if i >= args.warmup:
             vals.append(cb)
-    value = statistics.mean(v["value"] for v in vals)
-    ms_per_step = statistics.mean(v["sample_seconds"] for v in vals) * 1e3
+    seconds = sum(v["sample_seconds"] for v in vals)
+    labels_equiv = sum(v["labels_equiv_per_sample"] for v in vals)
+    value = labels_equiv / seconds  # == labels_per_step / (ms_per_step / 1e3)
     cb = dict(vals[-1])
     cb["value"] = value
+    cfg = workload_config(args, 1)
+    cfg.update({
+        "parallelism": f"{threads} host threads (one reference NetRunner per thread; SPEC.md:251,508)",
+        "labels_per_step": labels_equiv / len(vals),
+        "measured": (f"per step: {threads} concurrent reference forwards of {args.cpu_tile}x{args.cpu_tile}-label "
+                     f"tiles (input {args.cpu_tile + V}) of the workload image; labels_per_step = the "
+                     f"sample's FLOPs / the workload's FLOP per label (reference flop_estimate at the "
+                     f"128-px tile), i.e. the workload extrapolated from the measured FLOP rate"),
+        "exact_path": "the reference itself: naive fp64-accumulating gemm (tensor.hpp:151-169), one core per thread",
+    })
     line = {
         "impl": "reference",
         "metric": "labels/s",
@@ -194,13 +232,13 @@ def run_reference(args):
         "n_gpus": args.gpus,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms_per_step,
+        "ms_per_step": seconds / len(vals) * 1e3,
         "higher_is_better": True,
         "scaling": "weak",
         "vs_baseline": value / PUBLISHED_SK_LABELS_PER_S,
         "dtype": "f64",
         "data": "synthetic: Rng(55) u8 image, init_weights(sk.net, seed 1)",
-        "config": workload_config(args, 1),
+        "config": cfg,
         "cpu_baseline": cb,
         "e2e": {"value": value, "unit": "labels/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
@@ -490,7 +528,7 @@ def run_ours(args):
         line["tolerance_mode"] = tol
     if ws == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_baseline_obj(args.cpu_threads or os.cpu_count() or 1,
-                                                args.cpu_tile)
+                                                args.cpu_tile, args.size)
     if ws > 1:
         import torch.distributed as dist
 

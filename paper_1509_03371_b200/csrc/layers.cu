@@ -397,10 +397,17 @@ __global__ void softmax_stitch_kernel(const double* __restrict__ scores, int n_t
     const int y = static_cast<int>(px / w), x = static_cast<int>(px % w);
     const int tg = t0 + tile;
     const int b = tg / tpi, ti = tg - b * tpi;
-    const int oy = min(y_base + (ti / ntx) * w, H - w);
-    const int ox = min((ti % ntx) * w, W - w);
+    const int ty = ti / ntx, tx = ti - ty * ntx;
+    const int oy = min(y_base + ty * w, H - w);
+    const int ox = min(tx * w, W - w);
     const int Y = oy + y;
     if (Y < y_lo || Y >= y_hi) continue;
+    // Edge tiles snap inward and overlap their predecessors; the later tile wins
+    // (pipeline.hpp:662-672, 685-694). A pixel is written only by the last tile (row-major)
+    // covering it, so the planes do not depend on launch order even when the overlapping
+    // tiles' values differ (strided nets).
+    if (ty + 1 < tpi / ntx && Y >= min(y_base + (ty + 1) * w, H - w)) continue;
+    if (tx + 1 < ntx && ox + x >= min((tx + 1) * w, W - w)) continue;
     const double* s = scores + static_cast<long long>(tile) * C * splane + static_cast<long long>(y) * wp + x;
     // softmax (S = float), keeping the C probabilities in a small loop (recomputed exp)
     double m = s[0];

@@ -9,6 +9,8 @@ fixtures are the reference tests' own data.
     python tests/golden/make_golden.py small     # seconds: layers.npz, nets.npz
     python tests/golden/make_golden.py sk229     # ~10 min: full sk.net at 229 (pixelseg bench)
     python tests/golden/make_golden.py u572 usk692
+    python tests/golden/make_golden.py strided     # ~1 min: multi-tile u.net/usk.net process()
+    python tests/golden/make_golden.py skproc      # ~75 min: full sk.net process() 260x230
 
 Runs only where /root/reference exists (the dev container); the .npz files are committed.
 """
@@ -351,10 +353,64 @@ def cli():
     np.save(os.path.join(d, "expect_scan_probs.npy"), probs)
 
 
+# Reduced-channel u.net / usk.net (the configs' own topology, strided pools and upconvs) for
+# multi-tile process(). Odd image sizes make the snapped edge tiles start at an odd offset, so
+# overlapping tiles see the strided pools at the opposite parity and produce different values:
+# the planes then pin both the reference's tile origins and its later-tile-wins stitch
+# (pipeline.hpp:662-672, 685-694).
+U_FOUT = {"conv1": 4, "conv2": 4, "conv3": 8, "conv4": 8, "conv5": 16, "conv6": 16, "conv7": 32,
+          "conv8": 32, "conv9": 64, "conv10": 64, "conv11": 32, "conv12": 32, "conv13": 32,
+          "conv14": 16, "conv15": 16, "conv16": 16, "conv17": 8, "conv18": 8, "conv19": 8,
+          "conv20": 4, "conv21": 4, "conv22": 4, "ip1": 2}
+USK_FOUT = {"conv1": 8, "conv2": 8, "conv3": 16, "conv4": 16, "conv5": 16, "ip1": 64, "ip2": 32,
+            "conv6": 16, "conv7": 16, "conv8": 8, "ip3": 2}
+STRIDED = (("u", "u.net", U_FOUT, 0.0, 36, 184, 101, 97),
+           ("usk", "usk.net", USK_FOUT, 0.05, 40, 180, 97, 93))
+
+
+def strided():
+    f = {}
+    for key, cfg, fout, sigma, w, v, H, W in STRIDED:
+        text = open(os.path.join(CONFIGS, cfg)).read()
+        net = O.RefNet(text, seed=5, fout=fout, sigma=sigma)
+        img = O.Rng(61).index_u8(H * W).reshape(H, W)
+        lab, pr = net.process(img, w, v)
+        f[f"{key}_img"], f[f"{key}_labels"], f[f"{key}_probs"] = img, lab, pr
+        f[f"{key}_geom"] = np.array([w, v, H, W], np.int32)
+        print(key, "tiles", O.tile_offsets(H, w), O.tile_offsets(W, w),
+              "label histogram", np.bincount(lab.ravel(), minlength=2))
+    np.savez_compressed(os.path.join(OUT, "strided.npz"), **f)
+    print("strided.npz", len(f), "arrays")
+
+
+# Full-width sk.net process() at the CLI's tile (w=128, v=101) on a non-square image whose
+# right and bottom tiles snap inward. The GPU retiles it internally (one 230-px tile column)
+# and runs ip1 (K = 19200) on the int8 certify-or-recompute path, so this pins that path on
+# the full net against the reference's own process(). Weights: init_weights(sk, 1), the bench's.
+SKPROC = (128, 101, 260, 230)
+
+
+def skproc():
+    w, v, H, W = SKPROC
+    text = open(os.path.join(CONFIGS, "sk.net")).read()
+    net = O.RefNet(text, seed=1)
+    img = O.Rng(55).index_u8(H * W).reshape(H, W)
+    lab, pr = net.process(img, w, v)
+    np.savez_compressed(os.path.join(OUT, "skproc.npz"), img=img, labels=lab, probs=pr,
+                        geom=np.array(SKPROC, np.int32),
+                        labels_sha=np.frombuffer(sha(lab).encode(), np.uint8),
+                        probs_sha=np.frombuffer(sha(pr).encode(), np.uint8))
+    print("skproc.npz written; labels", np.bincount(lab.ravel(), minlength=2))
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["small"]:
         if arg == "cli":
             cli()
+        elif arg == "strided":
+            strided()
+        elif arg == "skproc":
+            skproc()
         elif arg == "small":
             configs()
             small()
