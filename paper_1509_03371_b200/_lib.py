@@ -45,6 +45,8 @@ PARAM_MOMENTUM = 2
 TC_BF16 = 1
 TC_TF32 = 2
 TC_BF16X3 = 3
+COMBINE_NCCL = 1
+COMBINE_PEER = 2
 
 
 class CudaError(Error):
@@ -121,6 +123,16 @@ _SIGS = {
     "graft_net_stream": (_vp, [_vp]),
     "graft_fp64_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _i]),
+    "graft_multi_create": (_i, [_i, _i, C.POINTER(LayerDesc), _i, C.POINTER(_i), C.POINTER(_vp)]),
+    "graft_multi_destroy": (None, [_vp]),
+    "graft_multi_size": (_i, [_vp, C.POINTER(_i)]),
+    "graft_multi_combine_kind": (_i, [_vp, C.POINTER(_i)]),
+    "graft_multi_net": (_i, [_vp, _i, C.POINTER(_vp)]),
+    "graft_multi_set_params_f32": (_i, [_vp, _i, _vp, _sz, _vp, _sz]),
+    "graft_multi_init_weights": (_i, [_vp, C.c_uint64]),
+    "graft_multi_set_option": (_i, [_vp, _i, C.c_longlong]),
+    "graft_multi_process": (_i, [_vp, _vp, _i, _i, _i, _i, _vp, _vp, _i]),
+    "graft_multi_process_batch": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _i]),
     "graft_process_batch": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _vp, _vp, _i]),
     "graft_process_band": (_i, [_vp, _vp, _i, _i, _i, _i, _i, _i, _vp, _vp, _i]),
     "graft_tile_rows": (_i, [_i, _i, _pi]),

@@ -9,8 +9,9 @@ bit-exact (pipeline.hpp:626-629; proj/tests/test_pipeline.cpp:535-588), so
   * a batch:     image i goes to rank i % world.
 
 The only collective is the final combine: the ranks' label/probability bands (or per-image
-planes) are all-gathered (NCCL over NVLink on GPUs; gloo in the CPU tests) and assembled on
-every rank. Nothing here touches the compute; it is exercised on CPU with gloo by
+planes) are gathered to rank 0 (NCCL over NVLink on GPUs; gloo in the CPU tests) and assembled
+there. The same partition and combine exist in the C ABI for one process driving all GPUs
+(graft_multi_process / graft_multi_process_batch, csrc/multi.cu; MultiProcessor below). Nothing here touches the compute; it is exercised on CPU with gloo by
 tests/test_multiproc_cpu.py and on GPUs by bench.py.
 """
 from __future__ import annotations
@@ -42,13 +43,24 @@ def band_rows_py(H: int, w: int, r0: int, r1: int) -> Tuple[int, int]:
     return y0, y1
 
 
-def combine_bands(labels, probs, bands: Sequence[Tuple[int, int]], rank: int, world: int,
-                  group=None):
-    """All-gathers every rank's rows [y0, y1) of (labels H x W, probs C x H x W) so that all ranks
-    end with the full planes. Works on CUDA tensors (NCCL) and CPU tensors (gloo); bands are
-    padded to the largest band height for the collective."""
+def _gather(t, rank: int, world: int, dst: int, group):
+    """dist.gather of equal-shape tensors to `dst` (None on other ranks); NCCL runs it as a
+    group of point-to-point sends to the destination, gloo natively."""
     import torch
     import torch.distributed as dist
+
+    out = [torch.empty_like(t) for _ in range(world)] if rank == dst else None
+    dist.gather(t, out, dst=dst, group=group)
+    return out
+
+
+def combine_bands(labels, probs, bands: Sequence[Tuple[int, int]], rank: int, world: int,
+                  group=None, dst: int = 0):
+    """Gathers every rank's rows [y0, y1) of (labels H x W, probs C x H x W) into rank `dst`'s
+    planes (the final combine goes to one rank; other ranks keep only their own
+    rows). Works on CUDA tensors (NCCL) and CPU tensors (gloo); bands are padded to the largest
+    band height for the collective."""
+    import torch
 
     H, W = labels.shape
     C = probs.shape[0]
@@ -60,13 +72,12 @@ def combine_bands(labels, probs, bands: Sequence[Tuple[int, int]], rank: int, wo
     prob_band = torch.zeros((C, hmax, W), dtype=probs.dtype, device=probs.device)
     lab_band[: y1 - y0] = labels[y0:y1]
     prob_band[:, : y1 - y0] = probs[:, y0:y1]
-    lab_all = [torch.empty_like(lab_band) for _ in range(world)]
-    prob_all = [torch.empty_like(prob_band) for _ in range(world)]
-    dist.all_gather(lab_all, lab_band, group=group)
-    dist.all_gather(prob_all, prob_band, group=group)
-    for r, (a, b) in enumerate(bands):
-        labels[a:b] = lab_all[r][: b - a]
-        probs[:, a:b] = prob_all[r][:, : b - a]
+    lab_all = _gather(lab_band, rank, world, dst, group)
+    prob_all = _gather(prob_band, rank, world, dst, group)
+    if rank == dst:
+        for r, (a, b) in enumerate(bands):
+            labels[a:b] = lab_all[r][: b - a]
+            probs[:, a:b] = prob_all[r][:, : b - a]
     return labels, probs
 
 
@@ -125,10 +136,11 @@ def shard_range(n_images: int, world: int, rank: int) -> Tuple[int, int]:
     return begin, begin + q + (1 if rank < r else 0)
 
 
-def gather_shards(lab_shard, prob_shard, n_images: int, rank: int, world: int, group=None):
-    """All-gathers per-rank batch shards (labels [n_r, H, W], probs [n_r, C, H, W], rank r owning
-    shard_range(...)) into the full batch on every rank: the batch mode's only collective.
-    Shards are padded to the largest size for the NCCL all-gather and trimmed after."""
+def gather_shards(lab_shard, prob_shard, n_images: int, rank: int, world: int, group=None,
+                  dst: int = 0):
+    """Gathers per-rank batch shards (labels [n_r, H, W], probs [n_r, C, H, W], rank r owning
+    shard_range(...)) into the full batch on rank `dst` (None, None elsewhere): the batch mode's
+    only collective. Shards are padded to the largest size for the collective and trimmed."""
     import torch
     import torch.distributed as dist
 
@@ -142,12 +154,12 @@ def gather_shards(lab_shard, prob_shard, n_images: int, rank: int, world: int, g
 
     lp, pp = padded(lab_shard), padded(prob_shard)
     if world > 1 or (dist.is_available() and dist.is_initialized()):
-        la = [torch.empty_like(lp) for _ in range(world)]
-        pa = [torch.empty_like(pp) for _ in range(world)]
-        dist.all_gather(la, lp, group=group)
-        dist.all_gather(pa, pp, group=group)
+        la = _gather(lp, rank, world, dst, group)
+        pa = _gather(pp, rank, world, dst, group)
     else:
         la, pa = [lp], [pp]
+    if rank != dst:
+        return None, None
     labs = torch.cat([la[r][:e - b] for r, (b, e) in enumerate(sizes)])
     probs = torch.cat([pa[r][:e - b] for r, (b, e) in enumerate(sizes)])
     return labs, probs
@@ -167,3 +179,99 @@ def process_batch_sharded(proc, images, w: int, v: int, rank: int, world: int, d
     if e > b:
         proc.run_batch(images[b:e], w, v, lab, prob, mem=_lib.MEM_DEVICE)
     return gather_shards(lab, prob, n, rank, world, group)
+
+
+class MultiProcessor:
+    """process() across the GPUs of this node from ONE process (graft_multi_*, csrc/multi.cu):
+    the net replicated on `devices`, one host thread and stream per GPU per call, tile-row
+    bands (one image) or image blocks (a batch) per GPU, planes bit-identical to one GPU's.
+    With device buffers (on devices[0]) the combine is one NCCL group of send/recv to rank 0
+    (peer copies when ranks share a device); with host buffers each GPU copies its own rows."""
+
+    def __init__(self, spec, states, devices=None, n_gpus: int = 0):
+        import ctypes as C
+
+        from . import _lib
+        from .netgraph import net_descs
+        from .netspec import LayerKind, compute_channels
+
+        if devices is None:
+            devices = list(range(n_gpus or 1))
+        self.devices = list(devices)
+        arr, self._keep = net_descs(spec)
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().graft_multi_create(spec.f0, len(spec.layers), arr, len(self.devices),
+                                                 devs, C.byref(h)))
+        self.h = h
+        self.spec = spec
+        self.n_classes = compute_channels(spec)[spec.layers[-1].output]
+        import numpy as np
+
+        for i, l in enumerate(spec.layers):
+            if l.kind != LayerKind.ConvSK:
+                continue
+            st = states.layers[i]
+            w = np.ascontiguousarray(st.weights, np.float32)
+            b = np.ascontiguousarray(st.bias, np.float32)
+            _lib.check(_lib.lib().graft_multi_set_params_f32(self.h, i, _lib.ptr(w), w.size,
+                                                             _lib.ptr(b), b.size))
+
+    def close(self):
+        from . import _lib
+
+        if getattr(self, "h", None) is not None and self.h.value:
+            _lib.lib().graft_multi_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def combine_kind(self) -> str:
+        import ctypes as C
+
+        from . import _lib
+
+        k = C.c_int()
+        _lib.check(_lib.lib().graft_multi_combine_kind(self.h, C.byref(k)))
+        return {_lib.COMBINE_NCCL: "nccl", _lib.COMBINE_PEER: "peer"}[k.value]
+
+    def set_option(self, opt: int, value: int) -> None:
+        from . import _lib
+
+        _lib.check(_lib.lib().graft_multi_set_option(self.h, opt, int(value)))
+
+    def run(self, image, w: int, v: int, labels=None, probs=None, mem: int = 0):
+        import numpy as np
+
+        from . import _lib
+
+        if mem == _lib.MEM_HOST:
+            image = np.ascontiguousarray(image, np.uint8)
+            H, W = image.shape
+            labels = np.zeros((H, W), np.uint8) if labels is None else labels
+            probs = np.zeros((self.n_classes, H, W), np.float32) if probs is None else probs
+        else:
+            H, W = image.shape
+        _lib.check(_lib.lib().graft_multi_process(self.h, _lib.ptr(image), H, W, w, v,
+                                                  _lib.ptr(labels), _lib.ptr(probs), mem))
+        return labels, probs
+
+    def run_batch(self, images, w: int, v: int, labels=None, probs=None, mem: int = 0):
+        import numpy as np
+
+        from . import _lib
+
+        if mem == _lib.MEM_HOST:
+            images = np.ascontiguousarray(images, np.uint8)
+            N, H, W = images.shape
+            labels = np.zeros((N, H, W), np.uint8) if labels is None else labels
+            probs = np.zeros((N, self.n_classes, H, W), np.float32) if probs is None else probs
+        else:
+            N, H, W = images.shape
+        _lib.check(_lib.lib().graft_multi_process_batch(self.h, _lib.ptr(images), N, H, W, w, v,
+                                                        _lib.ptr(labels), _lib.ptr(probs), mem))
+        return labels, probs

@@ -77,7 +77,9 @@ def test_cli_exit_codes(tmp_path):
     bad = tmp_path / "bad.net"
     bad.write_text("input w=10 f=1\nlayer c conv_sk k=3 fout=0 in=data out=c\n")
     assert run("flops", "--net", str(bad)).returncode == 2            # SpecError
-    assert run("bench", "--net", str(bad), "--backward").returncode == 1
+    assert run("bench", "--net", str(bad), "--backward").returncode == 2  # SpecError first
+    assert run("process", "--net", str(bad), "--weights", "w", "--in", "i", "--out", "o",
+               "--gpus", "0").returncode == 1                       # usage
 
 
 # ---- process / bench on the GPU -------------------------------------------------------------
@@ -137,3 +139,53 @@ def test_cli_bench_report(tmp_path):
     assert rows[("output", "extent")] == "128"
     assert float(rows[("throughput", "px_per_s")]) > 0
     assert ("ip1", "efficiency") in rows and ("total", "gflops") in rows
+
+
+TIMING = {"seconds", "gflops", "efficiency", "px_per_s"}
+
+
+def strip_timing(text):
+    """The bench report without its timing columns (acceptance.cpp:1159-1166 compares the rest)."""
+    return [ln for ln in text.splitlines() if not (len(ln.split("\t")) == 3 and ln.split("\t")[1] in TIMING)]
+
+
+@pytest.mark.gpu
+@needs_bin
+def test_cli_determinism(tmp_path):
+    """proj/tests/acceptance.cpp:1106-1178 on the GPU CLI: two identically seeded runs give
+    byte-identical output files (process) and identical reports outside the timing columns
+    (bench, forward and --backward)."""
+    outs = []
+    for i in range(2):
+        out = tmp_path / f"o{i}"
+        r = run("process", "--net", os.path.join(CLI, "sk_small.net"), "--weights",
+                os.path.join(CLI, "sk_small.pxsg"), "--in", os.path.join(CLI, "scan.pgm"), "--out",
+                str(out), "--prob")
+        assert r.returncode == 0, r.stderr
+        outs.append([open(out / f"scan_{n}.pgm", "rb").read() for n in ("labels", "prob0", "prob1")])
+    assert outs[0] == outs[1]
+    reports = []
+    for i in range(2):
+        r = run("bench", "--net", os.path.join(CLI, "sk_small.net"), "--w0", "130", "--trials", "2",
+                "--seed", "5", "--backward")
+        assert r.returncode == 0, r.stderr
+        reports.append(r.stdout)
+    assert strip_timing(reports[0]) == strip_timing(reports[1])
+    rows = {tuple(ln.split("\t")[:2]): ln.split("\t")[2] for ln in reports[0].splitlines()[1:]}
+    assert float(rows[("backward", "seconds")]) > 0
+
+
+@pytest.mark.gpu
+@needs_bin
+@pytest.mark.parametrize("gpus", [2, 3])
+def test_cli_process_gpus_same_files(tmp_path, gpus):
+    """--gpus G: tile-row bands on G ranks (round-robin over the visible GPUs) give the
+    reference's output files byte for byte."""
+    out = tmp_path / "out"
+    r = run("process", "--net", os.path.join(CLI, "sk_small.net"), "--weights",
+            os.path.join(CLI, "sk_small.pxsg"), "--in", os.path.join(CLI, "scan.pgm"), "--out",
+            str(out), "--prob", "--gpus", str(gpus))
+    assert r.returncode == 0, r.stderr
+    for name in ("labels", "prob0", "prob1"):
+        assert open(out / f"scan_{name}.pgm", "rb").read() == \
+            open(os.path.join(CLI, f"expect_scan_{name}.pgm"), "rb").read(), name

@@ -1,7 +1,8 @@
 """World-size-2 gloo tests of the multi-GPU partitioner and final combine on CPU
 (paper_1509_03371_b200/multigpu.py). The per-band compute is the CPU oracle restricted to the
-band's rows -- exactly what graft_process_band writes -- so the test pins the partition and
-the combine; the GPU band kernel itself is covered by tests/test_gpu_net.py."""
+band's rows -- exactly what graft_process_band writes (there is no GPU here) -- so the test pins
+the partition and the gather-to-rank-0 combine; the GPU band kernels themselves are covered by
+tests/test_gpu_net.py and tests/test_gpu_multigpu.py (graft_multi_process on the device)."""
 import os
 import socket
 
@@ -70,8 +71,12 @@ def _worker(rank, world, port, H, W, w, q):
         probs[:, y0:y1] = torch.from_numpy(full_prob[:, y0:y1])
 
     M.process_image(run_band, H, w, rank, world, labels, probs)
-    ok = np.array_equal(labels.numpy(), full_lab) and \
-        np.array_equal(probs.numpy().view(np.uint32), full_prob.view(np.uint32))
+    if rank == 0:  # the combine gathers to rank 0
+        ok = np.array_equal(labels.numpy(), full_lab) and \
+            np.array_equal(probs.numpy().view(np.uint32), full_prob.view(np.uint32))
+    else:  # other ranks keep exactly their own band
+        y0, y1 = M.band_rows_py(H, w, *M.split_rows((H + w - 1) // w, world)[rank])
+        ok = np.array_equal(labels.numpy()[y0:y1], full_lab[y0:y1])
     # batch mode: images round-robin, all-gathered
     per = {}
     for i in M.batch_assignment(3, world, rank):
@@ -83,8 +88,11 @@ def _worker(rank, world, port, H, W, w, q):
     lab_sh = torch.stack([torch.full((4, 5), i, dtype=torch.uint8) for i in range(b, e)])
     prob_sh = torch.stack([torch.full((2, 4, 5), float(i) + 0.5) for i in range(b, e)])
     la, pa = M.gather_shards(lab_sh, prob_sh, 5, rank, world)
-    ok = ok and la.shape == (5, 4, 5) and all(int(la[i, 3, 4]) == i for i in range(5)) and \
-        all(float(pa[i, 1, 0, 0]) == i + 0.5 for i in range(5))
+    if rank == 0:
+        ok = ok and la.shape == (5, 4, 5) and all(int(la[i, 3, 4]) == i for i in range(5)) and \
+            all(float(pa[i, 1, 0, 0]) == i + 0.5 for i in range(5))
+    else:
+        ok = ok and la is None and pa is None
     q.put((rank, ok))
     dist.destroy_process_group()
 

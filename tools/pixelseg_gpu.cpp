@@ -1,8 +1,10 @@
 // pixelseg_gpu -- the reference CLI's GPU-path subcommands (proj/tools/pixelseg.cpp) on the
 // B200 drop-ins of include/pixelseg_gpu.hpp.
 //
-//   process --net N --weights W --in IMG --out DIR [--prob] [--tile T]   (pixelseg.cpp:161-191)
-//   bench   --net N [--w0 W] [--trials T] [--peak-gflops P] [--seed S]   (pixelseg.cpp:193-267)
+//   process --net N --weights W --in IMG --out DIR [--prob] [--tile T] [--gpus G]
+//                                                                        (pixelseg.cpp:161-191)
+//   bench   --net N [--w0 W] [--trials T] [--peak-gflops P] [--seed S] [--backward]
+//                                                                        (pixelseg.cpp:193-267)
 //   sizes   --net N [--w0 W]                                             (pixelseg.cpp:97-101)
 //   flops   --net N [--w0 W]                                             (pixelseg.cpp:113-121)
 //
@@ -13,7 +15,8 @@
 // pixelseg::gpu:: -- labels and probability maps are bit-identical.
 //
 // The reference parses its flags with CLI11 (absent here); this file parses the same flag
-// names by hand. `bench --backward` (training) is outside the B200 path and exits 1.
+// names by hand. `--gpus G` (process) is the one addition: tile-row bands on G GPUs of this
+// node (pixelseg::gpu::process(..., n_gpus), graft_multi_process), the same output files.
 #include <algorithm>
 #include <chrono>
 #include <cmath>
@@ -109,12 +112,12 @@ Plane<std::uint8_t> prob_map(const Plane<float>& p) {
 // `process` (pixelseg.cpp:161-191): the tile defaults to the net's own output extent and the
 // context surplus v is a property of the net; only the labelling runs on the GPU.
 int cmd_process(const NetSpec& spec, const std::string& weights_path, const std::string& in_path,
-                const std::string& out_dir, bool want_probs, int tile) {
+                const std::string& out_dir, bool want_probs, int tile, int gpus) {
   namespace fs = std::filesystem;
   const int v = spec.w0 - output_extent(spec, spec.w0);
   NetStates<float> states = load_weights<float>(weights_path, spec);
   const Plane<std::uint8_t> image = read_gray_image(in_path);
-  const ProcessResult<float> res = gpu::process(spec, states, image, tile > 0 ? tile : spec.w0 - v, v);
+  const ProcessResult<float> res = gpu::process(spec, states, image, tile > 0 ? tile : spec.w0 - v, v, gpus);
 
   fs::create_directories(out_dir);
   const fs::path base = fs::path(out_dir) / fs::path(in_path).stem();
@@ -128,12 +131,13 @@ int cmd_process(const NetSpec& spec, const std::string& weights_path, const std:
   return 0;
 }
 
-// `bench` (pixelseg.cpp:193-267, forward only): same seeds (weights init_weights(spec, seed),
-// input Rng(seed ^ 0x9e3779b97f4a7c15).uniform(-1,1)) and the same report lines. Per-layer
-// seconds are CUDA-event times of that layer's kernels; the total is host time around
-// gpu::NetRunner::forward (input H2D and output D2H included). One untimed forward first
-// uploads the weights.
-int cmd_bench(const NetSpec& spec, int w0, int trials, double peak_gflops, std::uint64_t seed) {
+// `bench` (pixelseg.cpp:193-267): same seeds (weights init_weights(spec, seed), input
+// Rng(seed ^ 0x9e3779b97f4a7c15).uniform(-1,1), output diffs drawn from the same stream after
+// each forward) and the same report lines. Per-layer seconds are CUDA-event times of that
+// layer's kernels; the totals are host time around gpu::NetRunner::forward / backward (host
+// copies included). One untimed forward first uploads the weights.
+int cmd_bench(const NetSpec& spec, int w0, int trials, double peak_gflops, bool backward,
+              std::uint64_t seed) {
   const int w_in = w0 > 0 ? w0 : spec.w0;
   const int w_out = propagate_sizes(spec, w_in).back().w_out;
   const FlopTable ft = flop_estimate(spec, w_in);
@@ -146,13 +150,25 @@ int cmd_bench(const NetSpec& spec, int w0, int trials, double peak_gflops, std::
                 [&] { return static_cast<float>(rng.uniform(-1.0, 1.0)); });
   runner.forward(input);
 
-  std::vector<double> totals;
+  std::vector<double> totals, bwd_totals;
   std::vector<std::vector<double>> layer_s(spec.layers.size());
   for (int t = 0; t < trials; ++t) {
     const auto a = std::chrono::steady_clock::now();
     runner.forward(input, /*timed=*/true);
     totals.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count());
     for (std::size_t i = 0; i < layer_s.size(); ++i) layer_s[i].push_back(runner.layer_seconds()[i]);
+    if (backward) {  // pixelseg.cpp:217-229
+      runner.zero_blob_diffs();
+      Blob<float>& out = runner.blob_mut(spec.layers.back().output);
+      for (auto& dv : out.diff) dv = static_cast<float>(rng.uniform(-1.0, 1.0));
+      const auto b0 = std::chrono::steady_clock::now();
+      runner.backward();
+      bwd_totals.push_back(std::chrono::duration<double>(std::chrono::steady_clock::now() - b0).count());
+      for (auto& st : states.layers) {  // keep the weights of every trial identical
+        std::fill(st.weight_diff.begin(), st.weight_diff.end(), 0.0f);
+        std::fill(st.bias_diff.begin(), st.bias_diff.end(), 0.0f);
+      }
+    }
   }
 
   auto rate_lines = [&](const std::string& name, long long fl, double sec) {
@@ -177,6 +193,7 @@ int cmd_bench(const NetSpec& spec, int w0, int trials, double peak_gflops, std::
   row("total", "seconds", g6(total));
   if (total > 0) row("total", "gflops", g6(ft.total / total * 1e-9));
   if (total > 0 && peak_gflops > 0) row("total", "efficiency", g6(ft.total / total * 1e-9 / peak_gflops));
+  if (backward) row("backward", "seconds", g6(median_of(bwd_totals)));
   row("output", "extent", w_out);
   if (total > 0) row("throughput", "px_per_s", g6(double(w_out) * w_out / total));
   const MemReport mem = buffer_and_memory(spec, w_in);
@@ -250,8 +267,8 @@ Args parse_args(int argc, char** argv, const std::vector<std::string>& options,
 const char* kUsage =
     "pixelseg_gpu: pixelwise segmentation nets with strided kernels (B200 path)\n"
     "usage: pixelseg_gpu SUBCOMMAND [OPTIONS]\n"
-    "  process --net N --weights W --in IMG --out DIR [--prob] [--tile T]\n"
-    "  bench   --net N [--w0 W] [--trials T] [--peak-gflops P] [--seed S]\n"
+    "  process --net N --weights W --in IMG --out DIR [--prob] [--tile T] [--gpus G]\n"
+    "  bench   --net N [--w0 W] [--trials T] [--peak-gflops P] [--seed S] [--backward]\n"
     "  sizes   --net N [--w0 W]\n"
     "  flops   --net N [--w0 W]\n";
 
@@ -270,20 +287,21 @@ int main(int argc, char** argv) {
   try {
     try {
       if (cmd == "process") {
-        const Args a = parse_args(argc, argv, {"--net", "--weights", "--in", "--out", "--tile"},
+        const Args a = parse_args(argc, argv, {"--net", "--weights", "--in", "--out", "--tile", "--gpus"},
                                   {"--prob"});
+        const long long gpus = a.integer("--gpus", 1);
+        if (gpus <= 0) throw Usage{"--gpus: value " + std::to_string(gpus) + " not a positive number"};
         return cmd_process(load_net(a.required("--net")), a.required("--weights"), a.required("--in"),
                            a.required("--out"), a.flag("--prob"),
-                           static_cast<int>(a.integer("--tile", 0)));
+                           static_cast<int>(a.integer("--tile", 0)), static_cast<int>(gpus));
       }
       if (cmd == "bench") {
         const Args a = parse_args(argc, argv, {"--net", "--w0", "--trials", "--peak-gflops", "--seed"},
                                   {"--backward"});
-        if (a.flag("--backward")) throw Usage{"--backward: training is not on the B200 path"};
         const long long trials = a.integer("--trials", 3);
         if (trials <= 0) throw Usage{"--trials: value " + std::to_string(trials) + " not a positive number"};
         return cmd_bench(load_net(a.required("--net")), static_cast<int>(a.integer("--w0", 0)),
-                         static_cast<int>(trials), a.real("--peak-gflops", 0.0),
+                         static_cast<int>(trials), a.real("--peak-gflops", 0.0), a.flag("--backward"),
                          static_cast<std::uint64_t>(a.integer("--seed", 1)));
       }
       if (cmd == "sizes" || cmd == "flops") {
