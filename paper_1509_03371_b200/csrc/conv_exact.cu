@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(32 * (WM * WN + NPROD), MINB) conv_ws_kernel(c
         for (int i = 0; i < TN; ++i) dmma(acc[j][i][0], acc[j][i][1], af, bf[i]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    release_stage(&empty[stage], lane);
   }
 
 #pragma unroll

@@ -227,8 +227,7 @@ __global__ void __launch_bounds__(32 * (WM * WN + 1), MINB)
         for (int i = 0; i < TN; ++i) dmma(acc[j][i][0], acc[j][i][1], af, bf[i]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[stage]);
+    release_stage(&empty[stage], lane);
   }
 
   // ---- epilogue: float(acc) + bias (fp32), optional relu -> pitched [b][m][oy][ox]

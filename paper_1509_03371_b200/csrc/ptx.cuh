@@ -41,6 +41,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// Consumer-side release of a shared-memory stage that an async copy (TMA / bulk copy /
+// cp.async) refills next: every lane's reads of the stage must be complete before the
+// arrive is observed. The arrive itself does not wait for the warp's in-flight LDS, and ptxas
+// schedules it above the DMMAs consuming those loads, so a refill could overwrite the stage
+// under a pending LDS (measured: wrong conv3 outputs under concurrent load). The proxy fence
+// orders this thread's earlier shared-memory reads (generic proxy) before the later async-proxy
+// writes and holds the lane until they have returned.
+__device__ __forceinline__ void release_stage(uint64_t* bar, int lane) {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncwarp();
+  if (lane == 0) mbar_arrive(bar);
+}
 // Non-blocking probe of a phase.
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, unsigned parity) {
   unsigned ok;
@@ -108,8 +120,15 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* tm, in
 // D[l/4][2*(l%4)+{0,1}]. Measured on this B200 (tools/fp64_probe.cu,
 // profiles/r01_fp64_probe.txt): the four products are added to D as the sequential fma chain
 // k0, k1, k2, k3 -- so a K loop of DMMAs in ascending k is the reference's ascending fp64 chain.
+//
+// volatile: the DMMAs stay in program order with the mbarrier arrive that releases their
+// operands' shared-memory stage. Without it the compiler hoisted the consumer's empty-barrier
+// arrive above the last k-group's DMMAs, i.e. between an LDS and the DMMA consuming it; the
+// arrive does not wait for the in-flight LDS, so the producer's TMA / cp.async refill could
+// land first and the DMMA read the next chunk's weights (seen under concurrent load: wrong
+// conv3 outputs in the last row group of the 64-row conv_tma kernel).
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d0), "+d"(d1)
       : "d"(a), "d"(b));
 }

@@ -264,8 +264,7 @@ __global__ void __launch_bounds__(288) gemm_tma_kernel(const __grid_constant__ C
         for (int y = 0; y < 4; ++y) dmma(acc[x][y][0], acc[x][y][1], af, bf[y]);
       }
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    release_stage(&empty[st], lane);
   }
 #pragma unroll
   for (int x = 0; x < 8; ++x) {
