@@ -244,12 +244,20 @@ class DeviceNet {
     shadow_[i].second = st.bias;
   }
 
+  // The reference's LayerState carries no generation number, so the check is a byte compare
+  // against the uploaded copy (memcmp: exact bits, so -0.0 vs +0.0 and NaN payloads count as
+  // changes; no copy unless something changed). Parameters changed by this library's own
+  // device-side updates are recorded through mark_synced without a compare.
+  static bool same_bits(const std::vector<float>& a, const std::vector<float>& b) {
+    return a.size() == b.size() && (a.empty() || std::memcmp(a.data(), b.data(), a.size() * sizeof(float)) == 0);
+  }
+
   void sync(const NetSpec& spec, const NetStates<float>& states) {
     for (std::size_t i = 0; i < spec.layers.size(); ++i) {
       if (spec.layers[i].kind != LayerKind::ConvSK) continue;
       const LayerState<float>& st = states.layers[i];
       auto& sh = shadow_[i];
-      if (sh.first == st.weights && sh.second == st.bias) continue;
+      if (same_bits(sh.first, st.weights) && same_bits(sh.second, st.bias)) continue;
       check(graft_net_set_params_f32(net_.get(), static_cast<int>(i), st.weights.data(),
                                      st.weights.size(), st.bias.data(), st.bias.size()));
       sh.first = st.weights;

@@ -15,6 +15,7 @@
 #include "pixelseg/convert.hpp"
 #include "pixelseg/image_io.hpp"
 #include "pixelseg/layers.hpp"
+#include "pixelseg/malis.hpp"
 #include "pixelseg/netgraph.hpp"
 #include "pixelseg/netspec.hpp"
 #include "pixelseg/pipeline.hpp"
@@ -499,4 +500,108 @@ void ref_sgd_step_f32(float* w, float* mom, float* diff, int n, double lr, doubl
   std::memcpy(diff, st.layers[0].weight_diff.data(), sizeof(float) * n);
 }
 
+// ---- MALIS (malis.hpp): affinity graph, components, maximin gradient, composed loss --------
+}  // extern "C"
+
+namespace {
+template <typename S>
+Plane<S> plane_of(const S* p, int h, int w) {
+  Plane<S> q(h, w);
+  std::memcpy(q.pix.data(), p, sizeof(S) * q.size());
+  return q;
+}
+template <typename S>
+void ref_affinity_forward(const S* fg, int h, int w, S* a_x, S* a_y, uint8_t* m_x, uint8_t* m_y) {
+  const AffinityGraph<S> g = affinity_forward(plane_of(fg, h, w));
+  std::memcpy(a_x, g.a_x.pix.data(), sizeof(S) * g.a_x.size());
+  std::memcpy(a_y, g.a_y.pix.data(), sizeof(S) * g.a_y.size());
+  std::memcpy(m_x, g.m_x.pix.data(), g.m_x.size());
+  std::memcpy(m_y, g.m_y.pix.data(), g.m_y.size());
+}
+template <typename S>
+int ref_affinity_backward(const S* da_x, const S* da_y, const uint8_t* m_x, const uint8_t* m_y, int h, int w,
+                          S* d_pos, S* d_neg) {
+  return guard([&] {
+    AffinityGraph<S> g(h, w);
+    std::memcpy(g.m_x.pix.data(), m_x, g.m_x.size());
+    std::memcpy(g.m_y.pix.data(), m_y, g.m_y.size());
+    Plane<S> dp, dn;
+    affinity_backward(plane_of(da_x, h, w), plane_of(da_y, h, w), g, dp, dn);
+    std::memcpy(d_pos, dp.pix.data(), sizeof(S) * dp.size());
+    std::memcpy(d_neg, dn.pix.data(), sizeof(S) * dn.size());
+  });
+}
+template <typename S>
+int ref_malis_gradient(const S* p_ax, const S* p_ay, const S* t_ax, const S* t_ay, const int* comp, int h, int w,
+                       S* da_x, S* da_y, long long* pos_x, long long* pos_y, long long* neg_x, long long* neg_y,
+                       long long* totals, double* losses) {
+  return guard([&] {
+    AffinityGraph<S> pred(h, w), truth(h, w);
+    pred.a_x = plane_of(p_ax, h, w);
+    pred.a_y = plane_of(p_ay, h, w);
+    truth.a_x = plane_of(t_ax, h, w);
+    truth.a_y = plane_of(t_ay, h, w);
+    const MalisResult<S> r = malis_gradient(pred, truth, plane_of(comp, h, w));
+    const size_t n = static_cast<size_t>(h) * w;
+    std::memcpy(da_x, r.da_x.pix.data(), sizeof(S) * n);
+    std::memcpy(da_y, r.da_y.pix.data(), sizeof(S) * n);
+    std::memcpy(pos_x, r.pos_x.pix.data(), sizeof(long long) * n);
+    std::memcpy(pos_y, r.pos_y.pix.data(), sizeof(long long) * n);
+    std::memcpy(neg_x, r.neg_x.pix.data(), sizeof(long long) * n);
+    std::memcpy(neg_y, r.neg_y.pix.data(), sizeof(long long) * n);
+    totals[0] = r.total_pos;
+    totals[1] = r.total_neg;
+    losses[0] = r.loss_pos;
+    losses[1] = r.loss_neg;
+    losses[2] = r.loss;
+  });
+}
+template <typename S>
+int ref_malis_softmax_loss(const S* scores, int C, int h, int w, const uint8_t* fg, S* diff, double* loss) {
+  return guard([&] {
+    Blob<S> s = make_blob(scores, C, h, w);
+    s.diff.assign(diff, diff + s.size());
+    *loss = malis_softmax_loss(s, plane_of(fg, h, w));
+    std::memcpy(diff, s.diff.data(), sizeof(S) * s.size());
+  });
+}
+}  // namespace
+
+extern "C" {
+void ref_affinity_forward_f32(const float* fg, int h, int w, float* ax, float* ay, uint8_t* mx, uint8_t* my) {
+  ref_affinity_forward(fg, h, w, ax, ay, mx, my);
+}
+void ref_affinity_forward_f64(const double* fg, int h, int w, double* ax, double* ay, uint8_t* mx, uint8_t* my) {
+  ref_affinity_forward(fg, h, w, ax, ay, mx, my);
+}
+int ref_affinity_backward_f32(const float* dax, const float* day, const uint8_t* mx, const uint8_t* my, int h,
+                              int w, float* dp, float* dn) {
+  return ref_affinity_backward(dax, day, mx, my, h, w, dp, dn);
+}
+int ref_affinity_backward_f64(const double* dax, const double* day, const uint8_t* mx, const uint8_t* my, int h,
+                              int w, double* dp, double* dn) {
+  return ref_affinity_backward(dax, day, mx, my, h, w, dp, dn);
+}
+void ref_connected_components(const uint8_t* labels, int h, int w, int* comp) {
+  const Plane<int> c = connected_components(plane_of(labels, h, w));
+  std::memcpy(comp, c.pix.data(), sizeof(int) * c.size());
+}
+int ref_malis_gradient_f32(const float* pax, const float* pay, const float* tax, const float* tay, const int* comp,
+                           int h, int w, float* dax, float* day, long long* px, long long* py, long long* nx,
+                           long long* ny, long long* totals, double* losses) {
+  return ref_malis_gradient(pax, pay, tax, tay, comp, h, w, dax, day, px, py, nx, ny, totals, losses);
+}
+int ref_malis_gradient_f64(const double* pax, const double* pay, const double* tax, const double* tay,
+                           const int* comp, int h, int w, double* dax, double* day, long long* px, long long* py,
+                           long long* nx, long long* ny, long long* totals, double* losses) {
+  return ref_malis_gradient(pax, pay, tax, tay, comp, h, w, dax, day, px, py, nx, ny, totals, losses);
+}
+int ref_malis_softmax_loss_f32(const float* scores, int C, int h, int w, const uint8_t* fg, float* diff,
+                               double* loss) {
+  return ref_malis_softmax_loss(scores, C, h, w, fg, diff, loss);
+}
+int ref_malis_softmax_loss_f64(const double* scores, int C, int h, int w, const uint8_t* fg, double* diff,
+                               double* loss) {
+  return ref_malis_softmax_loss(scores, C, h, w, fg, diff, loss);
+}
 }  // extern "C"

@@ -39,6 +39,8 @@ OPT_TC_KIND = 7
 OPT_TRAINING = 8
 OPT_CRT_MIN_K = 9
 OPT_CRT_FALLBACKS = 10
+OPT_STAGING_BUDGET = 4
+OPT_LAST_BANDS = 11
 PARAM_DIFF = 1
 PARAM_MOMENTUM = 2
 
@@ -166,6 +168,16 @@ _SIGS = {
     "graft_gemm_i8": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
     "graft_i8_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_conv_crt_f32": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i, _vp]),
+    "graft_net_malis_softmax_loss_f32": (_i, [_vp, C.c_char_p, _vp, _i, _i, C.POINTER(_d)]),
+    "graft_affinity_forward_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i]),
+    "graft_affinity_forward_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, _vp, _i]),
+    "graft_affinity_backward_f32": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i]),
+    "graft_affinity_backward_f64": (_i, [_vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _i]),
+    "graft_connected_components_u8": (_i, [_vp, _i, _i, _i, _vp, _i]),
+    "graft_malis_gradient_f32": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i]),
+    "graft_malis_gradient_f64": (_i, [_vp, _vp, _vp, _vp, _vp, _i, _i, _i, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _i]),
+    "graft_malis_softmax_loss_f32": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _i]),
+    "graft_malis_softmax_loss_f64": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _vp, _i]),
     "graft_launch_count": (C.c_longlong, []),
     "graft_reset_launch_count": (None, []),
 }

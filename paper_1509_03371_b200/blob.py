@@ -5,6 +5,7 @@ to the reference's ``std::vector`` so buffers pass straight to the C ABI.
 """
 from __future__ import annotations
 
+import itertools
 from typing import Optional
 
 import numpy as np
@@ -146,8 +147,41 @@ class ColumnBuffer:
         return self.data[r * self.cols + c]
 
 
+_GENERATION = itertools.count(1)
+
+
 class LayerState:
-    """LayerState<S> (layers.hpp:19-37)."""
+    """LayerState<S> (layers.hpp:19-37).
+
+    `weights` and `bias` carry a generation number that changes whenever either attribute is
+    assigned, so a device net re-uploads a layer's parameters only when its generation moved:
+    O(layers) per call instead of comparing every weight. Once uploaded, the arrays are marked
+    read-only; an in-place write (`st.weights[0] = x`) raises instead of leaving a stale device
+    copy. Change parameters by assignment (`st.weights = new_array`)."""
+
+    @property
+    def weights(self) -> np.ndarray:
+        return self._weights
+
+    @weights.setter
+    def weights(self, a) -> None:
+        self._weights = a
+        self.generation = next(_GENERATION)
+
+    @property
+    def bias(self) -> np.ndarray:
+        return self._bias
+
+    @bias.setter
+    def bias(self, a) -> None:
+        self._bias = a
+        self.generation = next(_GENERATION)
+
+    def freeze_params(self) -> None:
+        """Marks weights and bias read-only (called once they are resident on a device)."""
+        for a in (self._weights, self._bias):
+            if isinstance(a, np.ndarray):
+                a.flags.writeable = False
 
     def __init__(self, dtype=np.float32):
         self.dtype = np.dtype(dtype)

@@ -22,6 +22,9 @@ struct CrtScratch {
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double ms[4] = {0, 0, 0, 0};
   long long gemm_launches = 0;
+  // smallest scratch request (bytes) that cudaMalloc refused; requests at least this large go
+  // straight to the caller's conv_exact fallback instead of retrying the allocation every call
+  size_t refused_bytes = 0;
   ~CrtScratch() {
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);

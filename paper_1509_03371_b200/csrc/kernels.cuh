@@ -163,11 +163,20 @@ void normalize_u8(const uint8_t* img, size_t n, float* out, cudaStream_t st);
 // tile t belongs to image t / tiles_per_image.
 void build_tiles(const uint8_t* img, int H, int W, int v, int w, int ntx, int t0, int n_tiles,
                  int f0, double* out, cudaStream_t st, int wp = 0, int y_base = 0,
-                 int tiles_per_image = 0);
+                 int tiles_per_image = 0, int img_row0 = 0, long long img_plane = 0);
 // Softmax head + per-pixel argmax + stitch of the tiles' scores (n_tiles x C x w x w) into the
 // image planes: labels H x W (u8), probs C x H x W (f32); rows outside [y_lo, y_hi) skipped.
+// A window of the planes (streamed process()): the buffers hold rows [out_row0, ...) of each
+// plane, out_plane elements per plane (0: H * W). img_row0 / img_plane window the input image
+// the same way for build_tiles.
 void softmax_stitch(const double* scores, int n_tiles, int C, int w, int ntx, int t0, int H, int W,
                     int y_lo, int y_hi, uint8_t* labels, float* probs, cudaStream_t st, int wp = 0,
-                    int y_base = 0, int tiles_per_image = 0);
+                    int y_base = 0, int tiles_per_image = 0, int out_row0 = 0, long long out_plane = 0);
+
+// malis_softmax_loss (malis.hpp:311-346) for a batch of patches on device buffers (malis.cu):
+// scores / sdiff [B][2][h][w] (sdiff accumulated), fg [B][h][w] u8, losses [B].
+template <typename S>
+void malis_softmax_loss_device(const S* scores, S* sdiff, const uint8_t* fg, int B, int h, int w, double* losses,
+                               cudaStream_t st);
 
 }  // namespace graft

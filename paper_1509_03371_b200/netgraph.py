@@ -110,20 +110,25 @@ class DeviceNet:
         return int(v.value)
 
     def sync_params(self, spec: NetSpec, states: NetStates) -> None:
-        """Uploads every conv layer whose host weights/bias differ from the last upload."""
+        """Uploads every conv layer whose parameters were assigned since its last upload
+        (LayerState.generation; O(layers), no weight is read unless it changed)."""
         for i, l in enumerate(spec.layers):
             if l.kind != LayerKind.ConvSK:
                 continue
             st = states.layers[i]
+            if self._uploaded.get(i) == (id(st), st.generation):
+                continue
             w = np.ascontiguousarray(st.weights, np.float32)
             bb = np.ascontiguousarray(st.bias, np.float32)
-            prev = self._uploaded.get(i)
-            if prev is not None and prev[0].shape == w.shape and prev[1].shape == bb.shape \
-                    and np.array_equal(prev[0], w) and np.array_equal(prev[1], bb):
-                continue
             _lib.check(_lib.lib().graft_net_set_params_f32(self.h, i, _lib.ptr(w), w.size,
                                                            _lib.ptr(bb), bb.size))
-            self._uploaded[i] = (w.copy(), bb.copy())
+            self.mark_synced(i, st)
+
+    def mark_synced(self, i: int, st) -> None:
+        """Records st's current parameters as the device's (after an upload or a device-side
+        update) and freezes the host arrays."""
+        st.freeze_params()
+        self._uploaded[i] = (id(st), st.generation)
 
 
 class NetRunner:
@@ -233,7 +238,7 @@ class NetRunner:
                 _lib.check(_lib.lib().graft_net_get_params_f32(self.net.h, i, _lib.ptr(w),
                                                                _lib.ptr(b)))
                 st.weights, st.bias = w, b
-                self.net._uploaded[i] = (w.copy(), b.copy())
+                self.net.mark_synced(i, st)
 
     def backward(self) -> None:
         """NetRunner::backward (netgraph.hpp:88-98) on the device: reverse sweep over the blob

@@ -83,7 +83,7 @@ def test_crt_conv_bit_identical(case, relu):
 
 @pytest.mark.parametrize("chain", ["1", "2", "3"])
 def test_crt_chain_kernels(monkeypatch, chain):
-    """Both fallback kernels (per 32-pixel segment, per 1024-pixel row window) on real failures
+    """Every fallback kernel (segments, row windows, v3) on real failures
     and on every output forced through the chain."""
     case = (1, 192, 40, 88, 256, 10, 4, "pool")
     B, C, H, W, M, k, d, _ = case

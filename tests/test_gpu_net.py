@@ -290,3 +290,30 @@ def test_process_large_ragged_image_properties():
     assert_bitwise(prb[0], pr, "batch of one")
     assert np.array_equal(lab, (pr[1] > pr[0]).astype(np.uint8))
     assert np.abs(pr.astype(np.float64).sum(0) - 1.0).max() < 1e-6
+
+
+def test_param_upload_follows_generation():
+    """Weights re-upload when assigned (generation moved) and not otherwise; in-place writes to
+    uploaded weights raise. The per-call check reads no weight (O(layers))."""
+    import time
+
+    spec = sk_small()
+    states = g.init_weights(spec, 3)
+    x = g.Rng(17).uniform_array(3 * 110 * 110, -1.0, 1.0).reshape(3, 110, 110)
+    runner = g.NetRunner(spec, states)
+    out0 = runner.forward(g.Blob.from_array(x)).view().copy()
+    ip3 = [i for i, l in enumerate(spec.layers) if l.name == "ip3"][0]
+    with pytest.raises(ValueError):
+        states.layers[ip3].bias[0] = 1.0
+    b = states.layers[ip3].bias.copy()
+    b[0] = 5.0
+    states.layers[ip3].bias = b
+    out1 = runner.forward(g.Blob.from_array(x)).view().copy()
+    assert not np.array_equal(out0, out1)
+    params = {i: (states.layers[i].weights, states.layers[i].bias)
+              for i, l in enumerate(spec.layers) if l.has_weights()}
+    assert_bitwise(out1, O.forward_net(spec, params, x))
+    t0 = time.perf_counter()
+    for _ in range(1000):
+        runner.net.sync_params(spec, states)
+    assert time.perf_counter() - t0 < 0.5

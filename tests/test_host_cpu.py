@@ -101,3 +101,24 @@ def test_parse_issues_match_reference_wording():
     assert "line 3: unknown layer kind 'bogus'" in text
     assert "input blob 'zz' is not produced by any earlier layer" in text
     assert "relu cannot set fout" in text
+
+
+def test_layer_state_generation_tracking():
+    """Parameter assignment moves LayerState.generation; freeze_params (called once a layer is
+    resident on a device) turns in-place writes into errors instead of stale device copies."""
+    st = g.LayerState()
+    st.init_conv(4, 6)
+    g0 = st.generation
+    st.weights = np.ones(24, np.float32)
+    assert st.generation != g0
+    g1 = st.generation
+    st.bias = np.zeros(4, np.float32)
+    assert st.generation != g1
+    st.freeze_params()
+    with pytest.raises(ValueError):
+        st.weights[0] = 2.0
+    w = st.weights.copy()
+    w[0] = 2.0
+    g2 = st.generation
+    st.weights = w
+    assert st.generation != g2 and st.weights[0] == 2.0
