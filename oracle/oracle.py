@@ -60,6 +60,15 @@ _ORC_SIGS = {
     "orc_normalize_f32": (None, [_vp, _sz, _vp]),
     "orc_tile_offsets": (_i, [_i, _i, C.POINTER(_i), _i]),
     "orc_stitch_f32": (None, [_vp, _i, _i, _i, _i, _i, _i, _vp, _vp]),
+    "orc_affinity_forward_f32": (None, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "orc_affinity_forward_f64": (None, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "orc_affinity_backward_f32": (None, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "orc_affinity_backward_f64": (None, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "orc_connected_components": (None, [_vp, _i, _i, _vp]),
+    "orc_malis_gradient_f32": (None, [_vp] * 5 + [_i, _i] + [_vp] * 8),
+    "orc_malis_gradient_f64": (None, [_vp] * 5 + [_i, _i] + [_vp] * 8),
+    "orc_malis_softmax_loss_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, C.POINTER(_d)]),
+    "orc_malis_softmax_loss_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, C.POINTER(_d)]),
 }
 
 _REF_SIGS = {
@@ -109,6 +118,15 @@ _REF_SIGS = {
     "ref_softmax_loss_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d)]),
     "ref_sgd_step_f32": (None, [_vp, _vp, _vp, _i, _d, _d, _d]),
     "ref_write_pgm": (_i, [C.c_char_p, _vp, _i, _i]),
+    "ref_affinity_forward_f32": (None, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "ref_affinity_forward_f64": (None, [_vp, _i, _i, _vp, _vp, _vp, _vp]),
+    "ref_affinity_backward_f32": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "ref_affinity_backward_f64": (_i, [_vp, _vp, _vp, _vp, _i, _i, _vp, _vp]),
+    "ref_connected_components": (None, [_vp, _i, _i, _vp]),
+    "ref_malis_gradient_f32": (_i, [_vp] * 5 + [_i, _i] + [_vp] * 8),
+    "ref_malis_gradient_f64": (_i, [_vp] * 5 + [_i, _i] + [_vp] * 8),
+    "ref_malis_softmax_loss_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, C.POINTER(_d)]),
+    "ref_malis_softmax_loss_f64": (_i, [_vp, _i, _i, _i, _vp, _vp, C.POINTER(_d)]),
 }
 
 
@@ -488,3 +506,74 @@ def correct_sw(text: str) -> str:
     buf = C.create_string_buffer(1 << 16)
     _chk(ref().ref_correct_sw(text.encode(), buf, len(buf)), ref().ref_last_error)
     return buf.value.decode()
+
+
+# ---- MALIS (malis.hpp) ------------------------------------------------------------------------
+def _msfx(dtype):
+    return "f64" if np.dtype(dtype) == np.float64 else "f32"
+
+
+def malis_affinity_forward(img, lib="orc"):
+    """affinity_forward (malis.hpp:34-52) of one h x w plane: (a_x, a_y, m_x, m_y)."""
+    L = orc() if lib == "orc" else ref()
+    img = np.ascontiguousarray(img)
+    h, w = img.shape
+    ax, ay = np.empty_like(img), np.empty_like(img)
+    mx, my = np.empty((h, w), np.uint8), np.empty((h, w), np.uint8)
+    getattr(L, f"{lib}_affinity_forward_{_msfx(img.dtype)}")(p(img), h, w, p(ax), p(ay), p(mx), p(my))
+    return ax, ay, mx, my
+
+
+def malis_affinity_backward(dax, day, mx, my, lib="orc"):
+    L = orc() if lib == "orc" else ref()
+    dax, day = np.ascontiguousarray(dax), np.ascontiguousarray(day)
+    h, w = dax.shape
+    dp, dn = np.empty_like(dax), np.empty_like(dax)
+    getattr(L, f"{lib}_affinity_backward_{_msfx(dax.dtype)}")(p(dax), p(day), p(np.ascontiguousarray(mx)),
+                                                              p(np.ascontiguousarray(my)), h, w, p(dp), p(dn))
+    return dp, dn
+
+
+def malis_components(labels, lib="orc"):
+    L = orc() if lib == "orc" else ref()
+    labels = np.ascontiguousarray(labels, np.uint8)
+    h, w = labels.shape
+    comp = np.empty((h, w), np.int32)
+    getattr(L, f"{lib}_connected_components")(p(labels), h, w, p(comp))
+    return comp
+
+
+def malis_gradient(pax, pay, tax, tay, comp, lib="orc"):
+    """malis_gradient (malis.hpp:197-298): dict of da_x, da_y, pos_x, pos_y, neg_x, neg_y,
+    totals (pos, neg) and losses (pos, neg, total)."""
+    L = orc() if lib == "orc" else ref()
+    arrs = [np.ascontiguousarray(a) for a in (pax, pay, tax, tay)]
+    comp = np.ascontiguousarray(comp, np.int32)
+    h, w = comp.shape
+    dt = arrs[0].dtype
+    out = {k: np.empty((h, w), dt) for k in ("da_x", "da_y")}
+    out.update({k: np.empty((h, w), np.int64) for k in ("pos_x", "pos_y", "neg_x", "neg_y")})
+    totals, losses = np.zeros(2, np.int64), np.zeros(3, np.float64)
+    rc = getattr(L, f"{lib}_malis_gradient_{_msfx(dt)}")(
+        *[p(a) for a in arrs], p(comp), h, w, p(out["da_x"]), p(out["da_y"]), p(out["pos_x"]), p(out["pos_y"]),
+        p(out["neg_x"]), p(out["neg_y"]), p(totals), p(losses))
+    if lib == "ref" and rc:
+        raise OracleError(rc, ref().ref_last_error().decode())
+    out["totals"], out["losses"] = totals, losses
+    return out
+
+
+def malis_softmax_loss(scores, fg, diff=None, lib="orc"):
+    """malis_softmax_loss (malis.hpp:311-346): returns (loss, diff) with diff accumulated."""
+    L = orc() if lib == "orc" else ref()
+    scores = np.ascontiguousarray(scores)
+    nc, h, w = scores.shape
+    d = np.zeros_like(scores) if diff is None else np.ascontiguousarray(diff, scores.dtype).copy()
+    loss = _d()
+    rc = getattr(L, f"{lib}_malis_softmax_loss_{_msfx(scores.dtype)}")(
+        p(scores), nc, h, w, p(np.ascontiguousarray(fg, np.uint8)), p(d), C.byref(loss))
+    if rc:
+        err = (orc().orc_last_error() if lib == "orc" else ref().ref_last_error()).decode()
+        raise OracleError(rc, err)
+    return loss.value, d
+

@@ -454,3 +454,264 @@ void orc_stitch_f32(const float* tp, int C, int w, int oy, int ox, int H, int W,
       for (int c = 0; c < C; ++c) probs[(size_t)c * plane + o] = tp[(size_t)c * tplane + t];
     }
 }
+
+/* ---- MALIS (malis.hpp): affinity graph, components, maximin gradient, composed loss ----- */
+
+/* affinity_forward (malis.hpp:34-52): a = std::min(a, b), m = (b < a); unused last column /
+ * row keep a = 1, m = 0. */
+#define DEFINE_AFF_FWD(NAME, T)                                                              \
+  void NAME(const T* img, int h, int w, T* ax, T* ay, uint8_t* mx, uint8_t* my) {            \
+    for (int i = 0; i < h * w; ++i) { ax[i] = (T)1; ay[i] = (T)1; mx[i] = 0; my[i] = 0; }    \
+    for (int y = 0; y < h; ++y)                                                              \
+      for (int x = 0; x + 1 < w; ++x) {                                                      \
+        const T a = img[y * w + x], b = img[y * w + x + 1];                                  \
+        ax[y * w + x] = (b < a) ? b : a;                                                     \
+        mx[y * w + x] = (b < a) ? 1 : 0;                                                     \
+      }                                                                                      \
+    for (int y = 0; y + 1 < h; ++y)                                                          \
+      for (int x = 0; x < w; ++x) {                                                          \
+        const T a = img[y * w + x], b = img[(y + 1) * w + x];                                \
+        ay[y * w + x] = (b < a) ? b : a;                                                     \
+        my[y * w + x] = (b < a) ? 1 : 0;                                                     \
+      }                                                                                      \
+  }
+DEFINE_AFF_FWD(orc_affinity_forward_f32, float)
+DEFINE_AFF_FWD(orc_affinity_forward_f64, double)
+
+/* affinity_backward (malis.hpp:58-80): scatter in the reference's loop order. */
+#define DEFINE_AFF_BWD(NAME, T)                                                              \
+  void NAME(const T* dax, const T* day, const uint8_t* mx, const uint8_t* my, int h, int w,   \
+            T* dpos, T* dneg) {                                                              \
+    for (int i = 0; i < h * w; ++i) { dpos[i] = (T)0; dneg[i] = (T)0; }                      \
+    for (int y = 0; y < h; ++y)                                                              \
+      for (int x = 0; x + 1 < w; ++x) {                                                      \
+        const int t = y * w + x + mx[y * w + x];                                             \
+        dpos[t] += dax[y * w + x];                                                           \
+        dneg[t] -= dax[y * w + x];                                                           \
+      }                                                                                      \
+    for (int y = 0; y + 1 < h; ++y)                                                          \
+      for (int x = 0; x < w; ++x) {                                                          \
+        const int t = (y + my[y * w + x]) * w + x;                                           \
+        dpos[t] += day[y * w + x];                                                           \
+        dneg[t] -= day[y * w + x];                                                           \
+      }                                                                                      \
+  }
+DEFINE_AFF_BWD(orc_affinity_backward_f32, float)
+DEFINE_AFF_BWD(orc_affinity_backward_f64, double)
+
+/* connected_components (malis.hpp:84-111): breadth-first flood from each unlabelled nonzero
+ * pixel in raster order, 4-neighbours in the order up, down, left, right. */
+void orc_connected_components(const uint8_t* lab, int h, int w, int* comp) {
+  const int n = h * w;
+  int* queue = (int*)malloc(sizeof(int) * (n > 0 ? n : 1));
+  int next = 0;
+  for (int i = 0; i < n; ++i) comp[i] = 0;
+  for (int s = 0; s < n; ++s) {
+    if (!lab[s] || comp[s]) continue;
+    ++next;
+    int qh = 0, qt = 0;
+    queue[qt++] = s;
+    comp[s] = next;
+    while (qh < qt) {
+      const int p = queue[qh++], y = p / w, x = p % w;
+      const int ny[4] = {y - 1, y + 1, y, y}, nx[4] = {x, x, x - 1, x + 1};
+      for (int k = 0; k < 4; ++k) {
+        if (ny[k] < 0 || ny[k] >= h || nx[k] < 0 || nx[k] >= w) continue;
+        const int q = ny[k] * w + nx[k];
+        if (!lab[q] || comp[q]) continue;
+        comp[q] = next;
+        queue[qt++] = q;
+      }
+    }
+  }
+  free(queue);
+}
+
+/* PairTracker (malis.hpp:117-176): per set a sorted array of (component id, count). */
+typedef struct {
+  int* id;
+  long long* n;
+  int len, cap;
+} orc_idmap;
+
+static void idmap_merge(orc_idmap* a, orc_idmap* b, long long* pos, long long* bg) {
+  /* pair counts of joining a and b (pos: same id > 0; bg: same id <= 0), then a += b */
+  int* id = (int*)malloc(sizeof(int) * (size_t)(a->len + b->len));
+  long long* n = (long long*)malloc(sizeof(long long) * (size_t)(a->len + b->len));
+  int i = 0, j = 0, k = 0;
+  *pos = 0;
+  *bg = 0;
+  while (i < a->len || j < b->len) {
+    if (j >= b->len || (i < a->len && a->id[i] < b->id[j])) {
+      id[k] = a->id[i]; n[k++] = a->n[i++];
+    } else if (i >= a->len || b->id[j] < a->id[i]) {
+      id[k] = b->id[j]; n[k++] = b->n[j++];
+    } else {
+      if (a->id[i] > 0) *pos += a->n[i] * b->n[j];
+      else *bg += a->n[i] * b->n[j];
+      id[k] = a->id[i]; n[k++] = a->n[i++] + b->n[j++];
+    }
+  }
+  free(a->id); free(a->n); free(b->id); free(b->n);
+  a->id = id; a->n = n; a->len = k; a->cap = k;
+  b->id = NULL; b->n = NULL; b->len = 0; b->cap = 0;
+}
+
+typedef struct {
+  const void* val; /* edge values (float or double) */
+  int dbl;
+} orc_edge_cmp_ctx;
+static __thread orc_edge_cmp_ctx g_cmp;
+static int edge_cmp(const void* pa, const void* pb) {
+  const int i = *(const int*)pa, j = *(const int*)pb;
+  const double vi = g_cmp.dbl ? ((const double*)g_cmp.val)[i] : (double)((const float*)g_cmp.val)[i];
+  const double vj = g_cmp.dbl ? ((const double*)g_cmp.val)[j] : (double)((const float*)g_cmp.val)[j];
+  if (vi != vj) return vi > vj ? -1 : 1;
+  return i < j ? -1 : (i > j ? 1 : 0);
+}
+
+static int uf_root(int* parent, int v) {
+  while (parent[v] != v) {
+    parent[v] = parent[parent[v]];
+    v = parent[v];
+  }
+  return v;
+}
+
+/* malis_gradient (malis.hpp:197-298). Edge ids: horizontal edges in raster order, then
+ * vertical. Outputs zeroed first; totals[2], losses[3] = {pos, neg, total}. */
+#define DEFINE_MALIS(NAME, T, DBL)                                                           \
+  void NAME(const T* pax, const T* pay, const T* tax, const T* tay, const int* comp, int h,   \
+            int w, T* dax, T* day, long long* posx, long long* posy, long long* negx,        \
+            long long* negy, long long* totals, double* losses) {                            \
+    const int n = h * w, nx = h * (w > 0 ? w - 1 : 0), ne = nx + (h > 0 ? h - 1 : 0) * w;     \
+    for (int i = 0; i < n; ++i) {                                                            \
+      dax[i] = (T)0; day[i] = (T)0; posx[i] = posy[i] = negx[i] = negy[i] = 0;               \
+    }                                                                                        \
+    int *ea = (int*)malloc(sizeof(int) * (ne + 1)), *eb = (int*)malloc(sizeof(int) * (ne + 1)); \
+    int* epos = (int*)malloc(sizeof(int) * (ne + 1));                                        \
+    for (int y = 0, e = 0; y < h; ++y)                                                       \
+      for (int x = 0; x + 1 < w; ++x, ++e) { ea[e] = y * w + x; eb[e] = ea[e] + 1; epos[e] = ea[e]; } \
+    for (int y = 0, e = nx; y + 1 < h; ++y)                                                  \
+      for (int x = 0; x < w; ++x, ++e) { ea[e] = y * w + x; eb[e] = ea[e] + w; epos[e] = ea[e]; } \
+    T* val = (T*)malloc(sizeof(T) * (ne + 1));                                               \
+    int* order = (int*)malloc(sizeof(int) * (ne + 1));                                       \
+    long long* cnt = (long long*)malloc(sizeof(long long) * (ne + 1));                       \
+    double* graw = (double*)malloc(sizeof(double) * (ne + 1));                               \
+    int *parent = (int*)malloc(sizeof(int) * (n + 1)), *rnk = (int*)malloc(sizeof(int) * (n + 1)); \
+    long long* size = (long long*)malloc(sizeof(long long) * (n + 1));                       \
+    orc_idmap* maps = (orc_idmap*)calloc((size_t)n + 1, sizeof(orc_idmap));                  \
+    double loss[2] = {0, 0};                                                                 \
+    for (int pass = 0; pass < 2; ++pass) {                                                   \
+      const int positive = pass == 0;                                                        \
+      for (int e = 0; e < ne; ++e) {                                                         \
+        const T p = e < nx ? pax[epos[e]] : pay[epos[e]];                                    \
+        const T t = e < nx ? tax[epos[e]] : tay[epos[e]];                                    \
+        val[e] = positive ? ((t < p) ? t : p) : ((p < t) ? t : p);                            \
+        order[e] = e;                                                                        \
+        cnt[e] = 0;                                                                          \
+        graw[e] = 0.0;                                                                       \
+      }                                                                                      \
+      g_cmp.val = val;                                                                       \
+      g_cmp.dbl = DBL;                                                                       \
+      qsort(order, (size_t)ne, sizeof(int), edge_cmp);                                       \
+      for (int i = 0; i < n; ++i) {                                                          \
+        parent[i] = i; rnk[i] = 0; size[i] = 1;                                              \
+        free(maps[i].id); free(maps[i].n);                                                   \
+        maps[i].id = (int*)malloc(sizeof(int)); maps[i].n = (long long*)malloc(sizeof(long long)); \
+        maps[i].id[0] = comp[i]; maps[i].n[0] = 1; maps[i].len = maps[i].cap = 1;            \
+      }                                                                                      \
+      long long total = 0;                                                                   \
+      double loss_raw = 0.0;                                                                 \
+      for (int r = 0; r < ne; ++r) {                                                         \
+        const int e = order[r];                                                              \
+        int ra = uf_root(parent, ea[e]), rb = uf_root(parent, eb[e]);                        \
+        if (ra == rb) continue;                                                              \
+        const long long sa = size[ra], sb = size[rb];                                        \
+        if (rnk[ra] < rnk[rb]) { const int t = ra; ra = rb; rb = t; }                        \
+        long long pos, bg;                                                                   \
+        idmap_merge(&maps[ra], &maps[rb], &pos, &bg);                                        \
+        parent[rb] = ra;                                                                     \
+        if (rnk[ra] == rnk[rb]) ++rnk[ra];                                                   \
+        size[ra] = sa + sb;                                                                  \
+        const long long neg = sa * sb - pos - bg;                                            \
+        const long long c = positive ? pos : neg;                                            \
+        if (c == 0) continue;                                                                \
+        cnt[e] = c;                                                                          \
+        total += c;                                                                          \
+        const double a = (double)val[e];                                                     \
+        if (positive) {                                                                      \
+          loss_raw += (double)c * (1.0 - a) * (1.0 - a);                                     \
+          graw[e] = (double)c * (-2.0) * (1.0 - a);                                          \
+        } else {                                                                             \
+          loss_raw += (double)c * a * a;                                                     \
+          graw[e] = (double)c * 2.0 * a;                                                     \
+        }                                                                                    \
+      }                                                                                      \
+      const double norm = total > 0 ? 1.0 / (double)total : 0.0;                             \
+      for (int e = 0; e < ne; ++e) {                                                         \
+        if (cnt[e] == 0) continue;                                                           \
+        const int hz = e < nx;                                                               \
+        long long* counts = hz ? (positive ? posx : negx) : (positive ? posy : negy);        \
+        counts[epos[e]] = cnt[e];                                                            \
+        const T p = hz ? pax[epos[e]] : pay[epos[e]], t = hz ? tax[epos[e]] : tay[epos[e]];   \
+        if (positive ? (p <= t) : (p >= t)) {                                                \
+          T* da = hz ? dax : day;                                                            \
+          da[epos[e]] += (T)(graw[e] * norm);                                                \
+        }                                                                                    \
+      }                                                                                      \
+      totals[pass] = total;                                                                  \
+      loss[pass] = loss_raw * norm;                                                          \
+    }                                                                                        \
+    losses[0] = loss[0];                                                                     \
+    losses[1] = loss[1];                                                                     \
+    losses[2] = loss[0] + loss[1];                                                           \
+    for (int i = 0; i < n; ++i) { free(maps[i].id); free(maps[i].n); }                       \
+    free(maps); free(ea); free(eb); free(epos); free(val); free(order); free(cnt); free(graw); \
+    free(parent); free(rnk); free(size);                                                     \
+  }
+DEFINE_MALIS(orc_malis_gradient_f32, float, 0)
+DEFINE_MALIS(orc_malis_gradient_f64, double, 1)
+
+/* malis_softmax_loss (malis.hpp:311-346); diff [2][h][w] accumulated. */
+#define DEFINE_MALIS_LOSS(NAME, T, SOFTMAX, AFF, GRAD, BWD)                                   \
+  int NAME(const T* scores, int C, int h, int w, const uint8_t* fg, T* diff, double* loss) {  \
+    if (C != 2) return fail(ORC_ESIZE, "malis loss: needs exactly 2 score channels, got %d", C); \
+    const size_t n = (size_t)h * w, nn = n ? n : 1;                                          \
+    T* probs = (T*)malloc(sizeof(T) * 2 * nn);                                               \
+    T* ft = (T*)malloc(sizeof(T) * nn);                                                      \
+    T *pax = (T*)malloc(sizeof(T) * nn), *pay = (T*)malloc(sizeof(T) * nn);                  \
+    T *tax = (T*)malloc(sizeof(T) * nn), *tay = (T*)malloc(sizeof(T) * nn);                  \
+    T *dax = (T*)malloc(sizeof(T) * nn), *day = (T*)malloc(sizeof(T) * nn);                  \
+    T *dp = (T*)malloc(sizeof(T) * nn), *dn = (T*)malloc(sizeof(T) * nn);                    \
+    uint8_t *mx = (uint8_t*)malloc(nn), *my = (uint8_t*)malloc(nn), *tmx = (uint8_t*)malloc(nn), \
+            *tmy = (uint8_t*)malloc(nn);                                                     \
+    int* comp = (int*)malloc(sizeof(int) * nn);                                              \
+    long long* cnts = (long long*)malloc(sizeof(long long) * 4 * nn);                        \
+    long long totals[2];                                                                     \
+    double losses[3];                                                                        \
+    SOFTMAX(scores, 2, h, w, probs);                                                         \
+    for (size_t i = 0; i < n; ++i) ft[i] = fg[i] ? (T)1 : (T)0;                              \
+    AFF(probs + n, h, w, pax, pay, mx, my);                                                  \
+    AFF(ft, h, w, tax, tay, tmx, tmy);                                                       \
+    orc_connected_components(fg, h, w, comp);                                                \
+    GRAD(pax, pay, tax, tay, comp, h, w, dax, day, cnts, cnts + nn, cnts + 2 * nn,           \
+         cnts + 3 * nn, totals, losses);                                                     \
+    BWD(dax, day, mx, my, h, w, dp, dn);                                                     \
+    for (size_t px = 0; px < n; ++px) {                                                      \
+      const T g1 = dp[px] * (T)0.5, g0 = dn[px] * (T)0.5;                                    \
+      double mix = 0.0;                                                                      \
+      mix += (double)g0 * (double)probs[px];                                                 \
+      mix += (double)g1 * (double)probs[n + px];                                             \
+      diff[px] += (T)((double)probs[px] * ((double)g0 - mix));                               \
+      diff[n + px] += (T)((double)probs[n + px] * ((double)g1 - mix));                       \
+    }                                                                                        \
+    *loss = losses[2];                                                                       \
+    free(probs); free(ft); free(pax); free(pay); free(tax); free(tay); free(dax); free(day);  \
+    free(dp); free(dn); free(mx); free(my); free(tmx); free(tmy); free(comp); free(cnts);    \
+    return ORC_OK;                                                                           \
+  }
+DEFINE_MALIS_LOSS(orc_malis_softmax_loss_f32, float, orc_softmax_f32, orc_affinity_forward_f32,
+                  orc_malis_gradient_f32, orc_affinity_backward_f32)
+DEFINE_MALIS_LOSS(orc_malis_softmax_loss_f64, double, orc_softmax_f64, orc_affinity_forward_f64,
+                  orc_malis_gradient_f64, orc_affinity_backward_f64)

@@ -103,6 +103,27 @@ int orc_tile_offsets(int extent, int w, int* offs, int cap);
 void orc_stitch_f32(const float* tile_probs, int C, int w, int oy, int ox, int H, int W,
                     uint8_t* labels, float* probs);
 
+/* ---- MALIS (malis.hpp) ---- */
+void orc_affinity_forward_f32(const float* img, int h, int w, float* ax, float* ay, uint8_t* mx, uint8_t* my);
+void orc_affinity_forward_f64(const double* img, int h, int w, double* ax, double* ay, uint8_t* mx, uint8_t* my);
+void orc_affinity_backward_f32(const float* dax, const float* day, const uint8_t* mx, const uint8_t* my, int h,
+                               int w, float* dpos, float* dneg);
+void orc_affinity_backward_f64(const double* dax, const double* day, const uint8_t* mx, const uint8_t* my, int h,
+                               int w, double* dpos, double* dneg);
+void orc_connected_components(const uint8_t* lab, int h, int w, int* comp);
+void orc_malis_gradient_f32(const float* pax, const float* pay, const float* tax, const float* tay,
+                            const int* comp, int h, int w, float* dax, float* day, long long* posx,
+                            long long* posy, long long* negx, long long* negy, long long* totals,
+                            double* losses);
+void orc_malis_gradient_f64(const double* pax, const double* pay, const double* tax, const double* tay,
+                            const int* comp, int h, int w, double* dax, double* day, long long* posx,
+                            long long* posy, long long* negx, long long* negy, long long* totals,
+                            double* losses);
+int orc_malis_softmax_loss_f32(const float* scores, int C, int h, int w, const uint8_t* fg, float* diff,
+                               double* loss);
+int orc_malis_softmax_loss_f64(const double* scores, int C, int h, int w, const uint8_t* fg, double* diff,
+                               double* loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -16,6 +16,9 @@ from .netgraph import NetRunner, NetStates, SolverConfig, init_weights, sgd_step
 from .pipeline import (ProcessResult, Processor, band_rows, mirror_pad, normalize_image, process,
                        tile_rows)
 from .rng import Rng
+from . import malis
+from .malis import (AffinityGraph, MalisResult, affinity_backward, affinity_forward, connected_components,
+                    malis_gradient, malis_softmax_loss)
 
 __all__ = [
     "Error", "IoError", "NumericError", "SizeError", "SpecError", "Blob", "ColumnBuffer",
@@ -24,5 +27,7 @@ __all__ = [
     "parse_netspec_or_throw", "propagate_sizes", "conv_sk_forward", "gemm", "gemm_flops",
     "im2col_sk", "maxpool_sk_forward", "mergecrop_forward", "relu_forward", "softmax_forward",
     "upconv_forward", "NetRunner", "NetStates", "SolverConfig", "init_weights", "sgd_step", "ProcessResult", "Processor",
-    "band_rows", "mirror_pad", "normalize_image", "process", "tile_rows", "Rng",
+    "band_rows", "mirror_pad", "normalize_image", "process", "tile_rows", "Rng", "malis",
+    "AffinityGraph", "MalisResult", "affinity_backward", "affinity_forward", "connected_components",
+    "malis_gradient", "malis_softmax_loss",
 ]

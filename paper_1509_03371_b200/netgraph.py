@@ -257,6 +257,13 @@ class NetRunner:
                                                          C.byref(loss)))
         return loss.value
 
+    def malis_softmax_loss(self, scores: str, fg: np.ndarray) -> float:
+        """malis_softmax_loss (malis.hpp:311-346) on this runner's blob `scores`: the training
+        step's MALIS loss (pipeline.hpp:599-606); diff += gradient, on the device."""
+        from .malis import malis_softmax_loss_device
+
+        return malis_softmax_loss_device(self.net.h, scores, fg)
+
 
 class SolverConfig:
     """The SGD fields of SolverConfig (pipeline.hpp:324-339) that sgd_step reads."""

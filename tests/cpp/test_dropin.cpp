@@ -360,7 +360,59 @@ static void backward_layer_cases() {
   }
 }
 
+// MALIS (malis.hpp) vs proj/tests/test_malis.cpp-style random instances, both S.
+template <typename S>
+static void malis_cases() {
+  Rng rng(909);
+  for (int trial = 0; trial < 12; ++trial) {
+    const int h = 1 + static_cast<int>(rng.uniform_index(20)), w = 1 + static_cast<int>(rng.uniform_index(20));
+    Plane<std::uint8_t> fg(h, w);
+    for (auto& v : fg.pix) v = rng.coin() ? 1 : 0;
+    Plane<S> probs(h, w), fgt(h, w);
+    for (auto& v : probs.pix) v = static_cast<S>(rng.uniform(0.01, 0.99));
+    for (std::size_t i = 0; i < fg.size(); ++i) fgt.pix[i] = fg.pix[i] ? S(1) : S(0);
+    const auto pr = affinity_forward(probs), pg = gpu::affinity_forward(probs);
+    CHECK(same_bits(pr.a_x.pix, pg.a_x.pix) && same_bits(pr.a_y.pix, pg.a_y.pix) &&
+              same_bits(pr.m_x.pix, pg.m_x.pix) && same_bits(pr.m_y.pix, pg.m_y.pix),
+          "affinity_forward");
+    const auto tr = affinity_forward(fgt);
+    const Plane<int> cr = connected_components(fg), cg = gpu::connected_components(fg);
+    CHECK(same_bits(cr.pix, cg.pix), "connected_components");
+    const auto rr = malis_gradient(pr, tr, cr);
+    const auto rg = gpu::malis_gradient(pr, tr, cr);
+    CHECK(same_bits(rr.da_x.pix, rg.da_x.pix) && same_bits(rr.da_y.pix, rg.da_y.pix), "malis_gradient da");
+    CHECK(same_bits(rr.pos_x.pix, rg.pos_x.pix) && same_bits(rr.pos_y.pix, rg.pos_y.pix) &&
+              same_bits(rr.neg_x.pix, rg.neg_x.pix) && same_bits(rr.neg_y.pix, rg.neg_y.pix),
+          "malis_gradient pair counts");
+    CHECK(rr.total_pos == rg.total_pos && rr.total_neg == rg.total_neg && rr.loss == rg.loss &&
+              rr.loss_pos == rg.loss_pos && rr.loss_neg == rg.loss_neg,
+          "malis_gradient totals and losses");
+    Plane<S> dpr, dnr, dpg, dng;
+    affinity_backward(rr.da_x, rr.da_y, pr, dpr, dnr);
+    gpu::affinity_backward(rr.da_x, rr.da_y, pr, dpg, dng);
+    CHECK(same_bits(dpr.pix, dpg.pix) && same_bits(dnr.pix, dng.pix), "affinity_backward");
+    Blob<S> sr(2, h, w);
+    fill(sr.data, rng);
+    sr.ensure_diff();
+    fill(sr.diff, rng);
+    Blob<S> sg = sr;
+    const double lr = malis_softmax_loss(sr, fg), lg = gpu::malis_softmax_loss(sg, fg);
+    CHECK(lr == lg && same_bits(sr.diff, sg.diff), "malis_softmax_loss");
+  }
+  Blob<S> three(3, 2, 2);
+  Plane<std::uint8_t> fg(2, 2, 1);
+  std::string msg;
+  try {
+    gpu::malis_softmax_loss(three, fg);
+  } catch (const SizeError& e) {
+    msg = e.what();
+  }
+  CHECK(msg == "malis loss: needs exactly 2 score channels, got 3", "malis loss channel check");
+}
+
 int main() {
+  malis_cases<float>();
+  malis_cases<double>();
   train_cases();
   backward_layer_cases();
   conv_cases<float>();

@@ -11,6 +11,7 @@ fixtures are the reference tests' own data.
     python tests/golden/make_golden.py u572 usk692
     python tests/golden/make_golden.py strided     # ~1 min: multi-tile u.net/usk.net process()
     python tests/golden/make_golden.py skproc      # ~75 min: full sk.net process() 260x230
+    python tests/golden/make_golden.py malis       # seconds: MALIS (malis.hpp) instances
 
 Runs only where /root/reference exists (the dev container); the .npz files are committed.
 """
@@ -403,6 +404,47 @@ def skproc():
     print("skproc.npz written; labels", np.bincount(lab.ravel(), minlength=2))
 
 
+# MALIS instances (malis.hpp): per case an h x w foreground plane and predicted probabilities
+# (numpy default_rng(seed), inputs stored), through the reference's affinity_forward,
+# connected_components, malis_gradient, affinity_backward and malis_softmax_loss, in float and
+# double. Shapes cover the degenerate extents (1x1, 1xn, nx1) and multi-component patches.
+MALIS_CASES = [(1, 1), (1, 7), (9, 1), (2, 2), (5, 5), (6, 9), (16, 16), (31, 24), (48, 48)]
+
+
+def malis():
+    f = {}
+    for ci, (h, w) in enumerate(MALIS_CASES):
+        rng = np.random.default_rng(1000 + ci)
+        fg = (rng.random((h, w)) < 0.55).astype(np.uint8)
+        probs = rng.uniform(0.01, 0.99, (h, w))
+        scores = rng.uniform(-1.0, 1.0, (2, h, w))
+        diff0 = rng.uniform(-1.0, 1.0, (2, h, w))
+        dgx, dgy = rng.uniform(-1.0, 1.0, (h, w)), rng.uniform(-1.0, 1.0, (h, w))
+        key = f"c{ci}"
+        f[f"{key}_fg"] = fg
+        f[f"{key}_comp"] = O.malis_components(fg, "ref")
+        for dt in (np.float32, np.float64):
+            t = "f32" if dt == np.float32 else "f64"
+            pr = probs.astype(dt)
+            pax, pay, pmx, pmy = O.malis_affinity_forward(pr, "ref")
+            tax, tay, _, _ = O.malis_affinity_forward(fg.astype(dt), "ref")
+            g = O.malis_gradient(pax, pay, tax, tay, f[f"{key}_comp"], "ref")
+            f[f"{key}_{t}_probs"] = pr
+            for n, a in (("pax", pax), ("pay", pay), ("pmx", pmx), ("pmy", pmy), ("tax", tax), ("tay", tay)):
+                f[f"{key}_{t}_{n}"] = a
+            for n, a in g.items():
+                f[f"{key}_{t}_{n}"] = a
+            dp, dn = O.malis_affinity_backward(dgx.astype(dt), dgy.astype(dt), pmx, pmy, "ref")
+            f[f"{key}_{t}_dgx"], f[f"{key}_{t}_dgy"] = dgx.astype(dt), dgy.astype(dt)
+            f[f"{key}_{t}_dpos"], f[f"{key}_{t}_dneg"] = dp, dn
+            sc, d0 = scores.astype(dt), diff0.astype(dt)
+            loss, d = O.malis_softmax_loss(sc, fg, d0, "ref")
+            f[f"{key}_{t}_scores"], f[f"{key}_{t}_diff0"] = sc, d0
+            f[f"{key}_{t}_loss"], f[f"{key}_{t}_diff"] = np.array([loss]), d
+    np.savez_compressed(os.path.join(OUT, "malis.npz"), cases=np.array(MALIS_CASES, np.int32), **f)
+    print("malis.npz written:", len(MALIS_CASES), "cases")
+
+
 if __name__ == "__main__":
     for arg in sys.argv[1:] or ["small"]:
         if arg == "cli":
@@ -411,6 +453,8 @@ if __name__ == "__main__":
             strided()
         elif arg == "skproc":
             skproc()
+        elif arg == "malis":
+            malis()
         elif arg == "small":
             configs()
             small()

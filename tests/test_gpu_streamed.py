@@ -93,7 +93,7 @@ def test_streamed_full_sk_bench_image():
     states = g.init_weights(spec, 1)
     img = g.Rng(55).index_array_u8(1024 * 1024, 256).reshape(1024, 1024)
     lab0, pr0, _ = streamed(spec, states, img, 128, 101, 0)
-    lab, pr, nb = streamed(spec, states, img, 128, 101, 16 << 20)
+    lab, pr, nb = streamed(spec, states, img, 128, 101, 6 << 20)  # the planes alone are 10 MB
     assert nb >= 2
     assert np.array_equal(lab, lab0)
     assert_bitwise(pr, pr0, "sk.net 1024^2 streamed")

@@ -229,3 +229,29 @@ def test_oracle_vs_live_reference_random_geometries():
         assert O.ref().ref_conv_f32(O.p(x), fi, h, h, O.p(w), O.p(b), fo, k, d, s, p_,
                                     O.p(ref)) == 0
         assert_bitwise(out, ref, f"trial {t}")
+
+
+# ---- MALIS (malis.hpp): the C restatement against the reference-made fixtures ------------
+def test_oracle_malis_matches_reference_goldens():
+    from conftest import load_golden
+
+    gold = load_golden("malis.npz")
+    for ci, (h, w) in enumerate(gold["cases"]):
+        key = f"c{ci}"
+        fg = gold[f"{key}_fg"]
+        comp = O.malis_components(fg)
+        assert np.array_equal(comp, gold[f"{key}_comp"]), key
+        for t in ("f32", "f64"):
+            k = f"{key}_{t}"
+            pax, pay, pmx, pmy = O.malis_affinity_forward(gold[f"{k}_probs"])
+            for n, a in (("pax", pax), ("pay", pay), ("pmx", pmx), ("pmy", pmy)):
+                assert_bitwise(a, gold[f"{k}_{n}"], f"{k} {n}")
+            r = O.malis_gradient(pax, pay, gold[f"{k}_tax"], gold[f"{k}_tay"], comp)
+            for n in ("da_x", "da_y", "pos_x", "pos_y", "neg_x", "neg_y", "totals", "losses"):
+                assert_bitwise(r[n], gold[f"{k}_{n}"], f"{k} {n}")
+            dp, dn = O.malis_affinity_backward(gold[f"{k}_dgx"], gold[f"{k}_dgy"], pmx, pmy)
+            assert_bitwise(dp, gold[f"{k}_dpos"], f"{k} dpos")
+            assert_bitwise(dn, gold[f"{k}_dneg"], f"{k} dneg")
+            loss, d = O.malis_softmax_loss(gold[f"{k}_scores"], fg, gold[f"{k}_diff0"])
+            assert_bitwise(np.array([loss]), gold[f"{k}_loss"], f"{k} loss")
+            assert_bitwise(d, gold[f"{k}_diff"], f"{k} diff")
