@@ -10,7 +10,7 @@ ki, mi, vi = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric Val
 agg = defaultdict(lambda: defaultdict(float))
 cnt = defaultdict(int)
 for r in rows[hdr + 1:]:
-    name = r[ki].split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
+    name = r[ki].replace("<unnamed>", "anon").split("(")[0].split("<")[0].replace("void ", "").split("::")[-1]
     agg[name][r[mi]] += float(r[vi].replace(",", ""))
     if r[mi] == "gpu__time_duration.sum":
         cnt[name] += 1
