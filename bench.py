@@ -489,25 +489,26 @@ def run_ours(args):
         _lib.check(_lib.lib().graft_net_crt_stats(net, cms, ctypes.byref(cl)))
         if cl.value > 0:
             # ip1 on the int8 path: crt_gemm2_kernel dominates. Algorithmic int8 ops = 2*M*N*K with
-            # the layer's own K times (14 residue planes + the bound plane + the chain-chunk sum
+            # the layer's own K times (the residue planes + the bound plane + the chain-chunk sum
             # planes, each over 1/nchunk of K: nchunk = C / 64 for C = 192, conv_crt.cu crt_chunk_bytes)
+            moduli = proc.net.get_option(_lib.OPT_CRT_MODULI)
             gemm_ms = cms[1]
             c_ip1 = 192
             cq = (c_ip1 + 15) // 16 * 16
             kb = 64 if cq % 128 else 128
             nchunk = -(-cq // kb)
-            planes = 15 + (nchunk - 1) / nchunk
+            planes = moduli + 1 + (nchunk - 1) / nchunk
             ops = planes * ip1_flops_total
             achieved = ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
             traffic = traffic_note = None
-            tp = os.path.join(ROOT, "profiles", "r01_crt_gemm_ncu_full.json")
-            if os.path.exists(tp) and wi == 1024 and n_tiles * args.steps == cl.value:
-                with open(tp) as f:
-                    tj = json.load(f)
+            tp = os.path.join(ROOT, "profiles", "r02_crt_gemm_ncu_full.json")
+            tj = json.load(open(tp)) if os.path.exists(tp) else {}
+            if tj.get("moduli") == moduli and wi == 1024 and n_tiles * args.steps == cl.value:
                 traffic = tj.get("traffic_bytes_per_launch")
-                traffic_note = (f"dram read+write of one crt_gemm_kernel launch (ncu --set full, profiles/"
-                                f"r01_crt_gemm_ncu_full.json); algorithmic {tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.1f} GB "
-                                "(15 weight planes once, 15 activation planes once, residue bytes + bound words out)")
+                traffic_note = (f"dram read+write of one crt_gemm2_kernel launch (ncu --set full, profiles/"
+                                f"r02_crt_gemm_ncu_full.json); algorithmic {tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.1f} GB "
+                                f"({moduli + 1} weight planes once, {moduli + 1} activation planes once, residue bytes + "
+                                "bound and chunk-sum words out)")
             roofline = {
                 "bound": "tensor",
                 "pipe": "int8 tensor (tcgen05.mma kind::i8, UTCIMMA)",
@@ -519,7 +520,7 @@ def run_ours(args):
                 "frac": achieved / i8_peak if achieved else None,
                 "traffic": traffic,
                 "traffic_note": traffic_note,
-                "kernel": f"crt_gemm2_kernel (ip1: M=1024, K=19200, 15 full planes + {nchunk - 1} chunk-sum planes, {wi * wi} px per launch)",
+                "kernel": f"crt_gemm2_kernel (ip1: M=1024, K=19200, {moduli + 1} full planes + {nchunk - 1} chunk-sum planes, {wi * wi} px per launch)",
                 "ops_per_launch": ops / cl.value,
                 "ops_source": f"{planes:.3f} planes x flop_estimate(sk.net, internal tile + 101)['ip1'] (convert.hpp:308-322)",
                 "avg_launch_ms": gemm_ms / cl.value,

@@ -10,14 +10,14 @@ namespace graft {
 // Weights prepared once per upload: [15][Mp][k*k][Cp] int8 (14 residue planes + the u8 |w|
 // ceilings), per-row exponents and L1 norms, and the fixed-point widths chosen for K.
 struct CrtWeights {
-  DevBuf planes, ew, w1;
+  DevBuf planes, ew, w1, nw;
   int M = 0, C = 0, k = 0, bw = 0, bx = 0;
   bool valid = false;
 };
 // Per-launch scratch (grown on demand): activation residue planes, patch sums, residue /
 // bound outputs of the GEMMs, and a small misc block (max|x|, fallback count, overflow list).
 struct CrtScratch {
-  DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff, approx;
+  DevBuf xres, s1, x1, res, sabs, misc, fails, xf, tapoff, approx, s1n, x1n;
   // timed mode: device ms accumulated per stage (0 prep, 1 residue GEMMs, 2 certify, 3 chain)
   cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   double ms[4] = {0, 0, 0, 0};
@@ -32,6 +32,7 @@ struct CrtScratch {
 };
 
 int crt_padded_c(int C);
+int crt_num_moduli();
 bool conv_crt_eligible(const ConvShape& sh);
 void crt_prepare_weights(const float* w_f32, int M, int C, int k, CrtWeights& cw, cudaStream_t st);
 size_t crt_scratch_bytes_per_image(const ConvShape& sh);
