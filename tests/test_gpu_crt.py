@@ -52,6 +52,8 @@ CASES = [  # B, C, H, W, M, k, d, input kind
     (1, 130, 20, 300, 200, 3, 2, "signed"),   # Cp 256, Mp 256, OW 296 > 256 (two row segments)
     (1, 48, 30, 40, 128, 5, 2, "pool"),       # conv2-like
     (1, 1024, 6, 40, 512, 1, 1, "pool"),      # ip2-like 1x1, K = 1024
+    (1, 100, 20, 300, 256, 3, 8, "signed"),   # row-window GEMM: d = 8, two sub-chunks (last partial)
+    (2, 144, 70, 90, 128, 5, 16, "pool"),     # row-window GEMM: d = 16, box of 192 pixels, 3 sub-chunks
 ]
 
 
