@@ -496,7 +496,8 @@ def run_ours(args):
             c_ip1 = 192
             cq = (c_ip1 + 15) // 16 * 16
             kb = 64 if cq % 128 else 128
-            nchunk = -(-cq // kb)
+            ch = 32 if kb == 64 and -(-cq // 64) == 3 else kb  # conv_crt.cu crt_chain_ch
+            nchunk = -(-cq // ch)
             planes = moduli + 1 + (nchunk - 1) / nchunk
             ops = planes * ip1_flops_total
             achieved = ops / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
@@ -505,7 +506,7 @@ def run_ours(args):
             tj = json.load(open(tp)) if os.path.exists(tp) else {}
             if tj.get("moduli") == moduli and wi == 1024 and n_tiles * args.steps == cl.value:
                 traffic = tj.get("traffic_bytes_per_launch")
-                traffic_note = (f"dram read+write of one crt_gemm2_kernel launch (ncu --set full, profiles/"
+                traffic_note = (f"dram read+write of one residue-GEMM launch (ncu --set full, profiles/"
                                 f"r02_crt_gemm_ncu_full.json); algorithmic {tj.get('algorithmic_bytes_per_launch', 0) / 1e9:.1f} GB "
                                 f"({moduli + 1} weight planes once, {moduli + 1} activation planes once, residue bytes + "
                                 "bound and chunk-sum words out)")
@@ -520,7 +521,7 @@ def run_ours(args):
                 "frac": achieved / i8_peak if achieved else None,
                 "traffic": traffic,
                 "traffic_note": traffic_note,
-                "kernel": f"crt_gemm2_kernel (ip1: M=1024, K=19200, {moduli + 1} full planes + {nchunk - 1} chunk-sum planes, {wi * wi} px per launch)",
+                "kernel": f"crt_gemm_rw_kernel (ip1: M=1024, K=19200, {moduli + 1} full planes + {nchunk - 1} chunk-sum planes of 1/{nchunk} K, {wi * wi} px per launch)",
                 "ops_per_launch": ops / cl.value,
                 "ops_source": f"{planes:.3f} planes x flop_estimate(sk.net, internal tile + 101)['ip1'] (convert.hpp:308-322)",
                 "avg_launch_ms": gemm_ms / cl.value,

@@ -1341,6 +1341,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
                                                  sizeof(double) * 2 * C3_TK * C3_PX);
   __shared__ int s_pre[C3_SEGS + 1];
   __shared__ int s_cnt[C3_PX + 1];
+  __shared__ int s_m[C3_SLOTS][C3_THREADS];  // the pass's chain rows, for the cooperative copies
   const int nsx = (a.OW + FIN_PX - 1) / FIN_PX;
   const int ngrp = (nsx + C3_SEGS - 1) / C3_SEGS;
   const int grp = blockIdx.x % ngrp;
@@ -1410,7 +1411,9 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
         mm[c] = static_cast<int>(e >> PXB);
         pp[c] = static_cast<int>(e & PXM);
       }
+      s_m[c][tid] = mm[c];
     }
+    __syncthreads();
     auto issue = [&](int ch, int stage) {
       const int kc = ch * C3_TK;
       // patch: C3_TK taps x 64 pixels of f64, 8-byte copies (a tap's pixels are one row run)
@@ -1422,13 +1425,27 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
         const double* src = ok ? inrow + __ldg(a.tap_off_in + kk) + px : a.in;
         cp_async8_zfill(&sP[stage][t][px], src, ok);
       }
+      if (vec) {
+        // weight runs, cooperatively: consecutive lanes copy the 16-byte pieces of one chain's
+        // run, so a warp-wide copy touches 16 rows' lines instead of 32 (the L1 wavefronts of
+        // these scattered rows bound the kernel)
+        constexpr int PIECES = C3_TK / 4;
+#pragma unroll
+        for (int e = 0; e < C3_SLOTS * PIECES; ++e) {
+          const int idx = e * C3_THREADS + tid;
+          const int r = idx / PIECES, pc = idx % PIECES;
+          const int c = r / C3_THREADS, t = r % C3_THREADS;
+          const int m = s_m[c][t];
+          if (m < 0) continue;
+          cp_async16_zfill(&sW[stage][c][t][4 * pc], a.w + static_cast<long long>(m) * a.K + kc + 4 * pc,
+                           kc + 4 * pc < a.K);
+        }
+      }
 #pragma unroll
       for (int c = 0; c < C3_SLOTS; ++c) {
         if (mm[c] < 0) continue;
         const float* wr = a.w + static_cast<long long>(mm[c]) * a.K + kc;
         if (vec) {
-#pragma unroll
-          for (int v = 0; v < C3_TK / 4; ++v) cp_async16_zfill(&sW[stage][c][tid][4 * v], wr + 4 * v, kc + 4 * v < a.K);
         } else {
 #pragma unroll
           for (int t = 0; t < C3_TK; ++t) cp_async4_zfill(&sW[stage][c][tid][t], wr + t, kc + t < a.K);
@@ -1472,6 +1489,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
       }
       __syncthreads();  // stage st is refilled by the next iteration's issue
     }
+    __syncthreads();  // s_m is rewritten by the next pass
 #pragma unroll
     for (int c = 0; c < C3_SLOTS; ++c) {
       if (mm[c] < 0) continue;
