@@ -322,7 +322,7 @@ void conv_tma(const double* in, const double* w_tiled, const float* bias, const 
   int variant = forced;
   // measured (profiles/r01_conv_variants_tma.txt): 32-tap stages + 64x32 warp tiles best for
   // 128-row blocks; 64-row blocks when f_out is not a multiple of 128
-  if (variant < 0) variant = (sh.M % 128 == 0) ? 8 : 4;
+  if (variant < 0) variant = (sh.M % 128 == 0) ? 8 : (sh.M % 96 == 0 ? 9 : 4);
   const int BNv = (variant == 2) ? 64 : 128;
   // pixel patch R x CW (R*CW = BN): minimise padded output pixels, prefer wide rows on ties
   long long best = -1;
@@ -381,6 +381,12 @@ void conv_tma(const double* in, const double* w_tiled, const float* bias, const 
       } else {
         launch<64, 128, 16, 2, 4, 4, 2>(tm, a, st, n_tiles);
       }
+      break;
+    case 9:  // 96-row blocks (f_out a multiple of 96 but not of 128, e.g. conv3's 192): one launch
+      if (3 * stage_bytes(96, 32) + 64 <= 227 * 1024)
+        launch<96, 128, 32, 2, 4, 3, 1>(tm, a, st, n_tiles);
+      else
+        launch<96, 128, 16, 2, 4, 4, 1>(tm, a, st, n_tiles);
       break;
     case 5:  // 128 x 128, 8-tap stages, deep ring
       if (11 * stage_bytes(128, 8) + 200 <= 227 * 1024)
