@@ -6,7 +6,10 @@ agreement with the exact planes, and the reference's CPU rate on all host cores 
 once on a bounded sample (bench.cpu_reference_sample) and scaled by FLOP/label to each size's
 tiling (marked "extrapolated"). One JSON line per size.
 
-    python tools/sweep.py [--min 10] [--max 28] [--tc-max 30] [--cpu]
+    python tools/sweep.py [--min 10] [--max 30] [--tc-max 30] [--cpu]
+
+Each line also carries the nvidia-smi clock samples (median SM clock, throttle reasons) taken
+during that size's timed runs (bench.ClockSampler).
 """
 import argparse
 import json
@@ -23,7 +26,7 @@ import bench  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--min", type=int, default=10)
-ap.add_argument("--max", type=int, default=28)
+ap.add_argument("--max", type=int, default=30)
 ap.add_argument("--tc-max", type=int, default=30)
 ap.add_argument("--cpu", action="store_true")
 a = ap.parse_args()
@@ -45,9 +48,9 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 cpu = None
 if a.cpu:
     threads = os.cpu_count() or 1
-    labels, wall, flops, kind = bench.cpu_reference_sample(threads, 8)
-    cpu = {"flop_per_s": flops / wall, "threads": threads, "kind": kind,
-           "sample": f"{threads} threads x one 8x8-label sk.net forward, {wall:.1f} s"}
+    r = bench.cpu_reference_sample(threads, 8)
+    cpu = {"flop_per_s": r["flops"] / r["wall"], "threads": threads, "kind": r["kind"],
+           "sample": f"{threads} threads x one 8x8-label sk.net forward, {r['wall']:.1f} s"}
 
 
 def timed(proc, img_d, lab, prob, w):
@@ -74,6 +77,8 @@ for n in range(a.min, max(a.max, a.tc_max) + 1):
     lab_t = torch.empty_like(lab)
     prob_t = torch.empty_like(prob)
     line = {"log2_px": n, "H": H, "W": W, "tile": w}
+    clocks = bench.ClockSampler(0)
+    clocks.start()
     try:
         if n <= a.max:
             if H * W <= (1 << 22):
@@ -93,6 +98,7 @@ for n in range(a.min, max(a.max, a.tc_max) + 1):
                 line["tc_max_abs_prob_diff"] = (prob_t - prob).abs().max().item()
     except Exception as e:  # report and continue (e.g. out of memory at the largest sizes)
         line["error"] = str(e)[:200]
+    line["clocks"] = clocks.stop()
     if cpu:
         wi = w if min(H, W) >= w else min(H, W)
         fpl = g.flop_estimate(spec, wi + V)["total"] / (wi * wi)
