@@ -42,6 +42,7 @@ OPT_CRT_FALLBACKS = 10
 OPT_STAGING_BUDGET = 4
 OPT_LAST_BANDS = 11
 OPT_CRT_MODULI = 12
+OPT_CRT_TUNE_MIN_K = 13
 PARAM_DIFF = 1
 PARAM_MOMENTUM = 2
 
