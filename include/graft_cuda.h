@@ -282,6 +282,8 @@ int graft_softmax_loss_layer_f32(const float* scores, int C, int H, int W, const
 /* sgd_step (pipeline.hpp:483-500) on one parameter array. */
 int graft_sgd_step_f32(float* w, float* mom, float* diff, size_t n, double lr, double momentum,
                        double weight_decay, int mem);
+int graft_sgd_step_f64(double* w, double* mom, double* diff, size_t n, double lr, double momentum,
+                       double weight_decay, int mem);
 int graft_net_get_option(const graft_net* net, int option, long long* value);
 
 /* ---- multi-GPU process() (the caller is pipeline.hpp:630-698 /

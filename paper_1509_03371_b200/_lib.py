@@ -167,6 +167,7 @@ _SIGS = {
     "graft_softmax_backward_f32": (_i, [_vp, _vp, _i, _i, _i, _vp, _i]),
     "graft_softmax_loss_layer_f32": (_i, [_vp, _i, _i, _i, _vp, _vp, _vp, C.POINTER(_d), _i]),
     "graft_sgd_step_f32": (_i, [_vp, _vp, _vp, _sz, _d, _d, _d, _i]),
+    "graft_sgd_step_f64": (_i, [_vp, _vp, _vp, _sz, _d, _d, _d, _i]),
     "graft_gemm_i8": (_i, [_vp, _i, _vp, _i, _i, _i, _vp]),
     "graft_i8_peak": (_i, [_d, C.POINTER(_d)]),
     "graft_conv_crt_f32": (_i, [_vp, _i, _i, _i, _i, _vp, _vp, _i, _i, _i, _vp, _i, _vp]),

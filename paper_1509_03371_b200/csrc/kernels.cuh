@@ -114,6 +114,7 @@ void mergecrop_backward(const float* dout, long long n, float* da, cudaStream_t 
 void softmax_backward(const double* prob, int C, int H, int W, int wp, const float* dout, float* din,
                       cudaStream_t st);
 void sgd(float* w, float* mom, float* diff, long long n, float lr, float mu, float wd, cudaStream_t st);
+void sgd(double* w, double* mom, double* diff, long long n, double lr, double mu, double wd, cudaStream_t st);
 // softmax_loss (layers.hpp:269-307) over a [C][H][W] score blob (pitched): diff += gradient,
 // *loss (device) = the reference's loss; terms = H*W f64 scratch; n_count = unmasked pixels.
 void softmax_loss(const double* scores, int C, int H, int W, int wp, const int* labels,
