@@ -37,6 +37,7 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <type_traits>
 
 #include "common.cuh"
 #include "crt.cuh"
@@ -1650,9 +1651,25 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
     }
     __syncthreads();
     int loaded = 0;  // kernel rows [0, loaded) are in (or on their way to) the ring
+    // this thread's cooperative weight copies, fixed for the pass: global float offset of the
+    // 16-byte piece (chain row m, piece pc) and its shared-memory byte offset within a stage
+    constexpr int PIECES = TK / 4, NCOPY = C3_SLOTS * PIECES;
+    constexpr uint32_t STAGE_BYTES = sizeof(float) * C3_SLOTS * C3_THREADS * (TK + 4);
+    int woff[NCOPY];
+    uint32_t wsm[NCOPY];
+    bool wok[NCOPY];
+#pragma unroll
+    for (int e = 0; e < NCOPY; ++e) {
+      const int idx = e * C3_THREADS + tid;
+      const int r = idx / PIECES, pc = idx % PIECES;
+      const int c = r / C3_THREADS, t = r % C3_THREADS;
+      const int m = s_m[c][t];
+      wok[e] = m >= 0;
+      woff[e] = (m >= 0 ? m : 0) * a.K + 4 * pc;  // < 2^31: M * K <= 2^31 checked at launch
+      wsm[e] = smem_u32(&sW[0][c][t][4 * pc]);
+    }
     auto issue = [&](int ch, int stage) {
       const int kc = ch * TK;
-      // the kernel rows this chunk reaches that are not in the ring yet
       const int hi = min((kc + TK - 1) / KS, nrows - 1);
       for (int r = loaded; r <= hi; ++r) {
         const long long roff = (static_cast<long long>(r / KS) * a.H + static_cast<long long>(r % KS) * DS) * a.wp;
@@ -1663,31 +1680,48 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
         }
       }
       loaded = max(loaded, hi + 1);
-      constexpr int PIECES = TK / 4;
+      const uint32_t sbase = static_cast<uint32_t>(stage) * STAGE_BYTES;
 #pragma unroll
-      for (int e = 0; e < C3_SLOTS * PIECES; ++e) {
-        const int idx = e * C3_THREADS + tid;
-        const int r = idx / PIECES, pc = idx % PIECES;
-        const int c = r / C3_THREADS, t = r % C3_THREADS;
-        const int m = s_m[c][t];
-        if (m < 0) continue;
-        cp_async16_zfill(&sW[stage][c][t][4 * pc], a.w + static_cast<long long>(m) * a.K + kc + 4 * pc, kc + 4 * pc < a.K);
-      }
+      for (int e = 0; e < NCOPY; ++e)
+        if (wok[e])  // K % TK == 0: every piece of a chunk lies inside the row
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(wsm[e] + sbase),
+                       "l"(a.w + woff[e] + kc));
       cp_async_commit();
     };
-    issue(0, 0);
     const double* p0 = sR + pp[0];
     const double* p1 = sR + pp[1];
-    for (int ch = 0; ch < nchunks; ++ch) {
-      const int st = ch & 1;
-      if (ch + 1 < nchunks) issue(ch + 1, st ^ 1);
-      else cp_async_commit();
-      cp_async_wait<1>();
-      __syncthreads();
-      const int j = ch % G::NCH;
-      if (live[1]) c6_dispatch<KS, DS, true>(j, &sW[st][0][tid][0], &sW[st][1][tid][0], p0, p1, acc);
-      else if (live[0]) c6_dispatch<KS, DS, false>(j, &sW[st][0][tid][0], nullptr, p0, nullptr, acc);
-      __syncthreads();
+    const int nper = (nchunks + G::NCH - 1) / G::NCH;
+    // the chunk loop, unrolled over a period (every tap offset an immediate), for one or two
+    // live slots
+    auto run = [&](auto two_tag) {
+      constexpr bool TWO = decltype(two_tag)::value;
+      issue(0, 0);
+      for (int per = 0; per < nper; ++per) {
+#pragma unroll
+        for (int jj = 0; jj < G::NCH; ++jj) {
+          const int ch = per * G::NCH + jj;
+          if (ch >= nchunks) break;
+          const int st = ch & 1;
+          if (ch + 1 < nchunks) issue(ch + 1, st ^ 1);
+          else cp_async_commit();
+          cp_async_wait<1>();
+          __syncthreads();
+          c6_dispatch<KS, DS, TWO>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], p0, p1, acc);
+          __syncthreads();
+        }
+      }
+    };
+    if (live[1]) run(std::integral_constant<bool, true>());
+    else if (live[0]) run(std::integral_constant<bool, false>());
+    else {  // no chain in this warp: still take part in the copies and barriers
+      issue(0, 0);
+      for (int ch = 0; ch < nchunks; ++ch) {
+        if (ch + 1 < nchunks) issue(ch + 1, (ch & 1) ^ 1);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        __syncthreads();
+      }
     }
     __syncthreads();
 #pragma unroll
@@ -2225,7 +2259,7 @@ bool conv_crt(const double* in, const CrtWeights& cw, const float* w_f32, const 
       ensure_dynamic_smem(reinterpret_cast<const void*>(kernel), smem);
       kernel<<<static_cast<unsigned>(ngrid), C3_THREADS, smem, st>>>(fa);
     };
-    const bool c6_ok = chain_kind == 6 && K % 8 == 0;
+    const bool c6_ok = chain_kind == 6 && K % 8 == 0 && static_cast<long long>(Mp) * K < (1LL << 31);
     if (c6_ok && sh.k == 10 && sh.d == 8) {
       chain6(crt_chain6_kernel<10, 8>, c6_smem_bytes<10, 8>());
     } else if (c6_ok && sh.k == 8 && sh.d == 8) {
