@@ -1119,32 +1119,32 @@ __global__ void __launch_bounds__(FIN_THREADS, CRT_CERT2_MINB) crt_certify2_kern
     R.exp_ok = R.ew + ex > -900 && R.ew < 900 && ex < 900;
     return R;
   };
-  if ((a.OW & 3) == 0) {
-    for (int i = threadIdx.x; i < (FIN_PX / 4) * a.M; i += FIN_THREADS) {
-      const int m = i / (FIN_PX / 4), g = i % (FIN_PX / 4), ox0 = px0 + 4 * g;
+  if ((a.OW & 1) == 0) {
+    // two pixels per thread: the loads of a pair stay in flight together, and the smaller
+    // register footprint lets CRT_CERT2_MINB blocks share an SM (the kernel is load-latency bound)
+    for (int i = threadIdx.x; i < (FIN_PX / 2) * a.M; i += FIN_THREADS) {
+      const int m = i / (FIN_PX / 2), g = i % (FIN_PX / 2), ox0 = px0 + 2 * g;
       if (ox0 >= a.OW) continue;
       const CertRow R = row(m);
       const long long ro = (static_cast<long long>(b) * a.Mp + m) * plane_px + static_cast<long long>(oy) * a.OW + ox0;
       uint32_t wres[NMOD];
 #pragma unroll
-      for (int j = 0; j < NMOD; ++j) wres[j] = __ldg(reinterpret_cast<const uint32_t*>(a.res + j * mod_plane + ro));
-      const int4 sab = __ldg(reinterpret_cast<const int4*>(a.sabs + ro));
-      int4 ap[NCH > 1 ? NCH - 1 : 1];
+      for (int j = 0; j < NMOD; ++j) wres[j] = __ldg(reinterpret_cast<const unsigned short*>(a.res + j * mod_plane + ro));
+      const int2 sab = __ldg(reinterpret_cast<const int2*>(a.sabs + ro));
+      int2 ap[NCH > 1 ? NCH - 1 : 1];
 #pragma unroll
-      for (int q = 0; q + 1 < NCH; ++q) ap[q] = __ldg(reinterpret_cast<const int4*>(a.approx + q * mod_plane + ro));
+      for (int q = 0; q + 1 < NCH; ++q) ap[q] = __ldg(reinterpret_cast<const int2*>(a.approx + q * mod_plane + ro));
       const int4 xa = __ldg(reinterpret_cast<const int4*>(a.x1 + xrow + ox0));
-      const int4 xb = __ldg(reinterpret_cast<const int4*>(a.x1 + xrow + ox0 + 2));
-      const int4 xn = __ldg(reinterpret_cast<const int4*>(a.x1n + xrow + ox0));
+      const int2 xn = __ldg(reinterpret_cast<const int2*>(a.x1n + xrow + ox0));
 #pragma unroll 1
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < 2; ++k) {
         int32_t apx[NCH > 1 ? NCH - 1 : 1];
 #pragma unroll
-        for (int q = 0; q + 1 < NCH; ++q) apx[q] = k == 0 ? ap[q].x : k == 1 ? ap[q].y : k == 2 ? ap[q].z : ap[q].w;
-        const int32_t sv = k == 0 ? sab.x : k == 1 ? sab.y : k == 2 ? sab.z : sab.w;
-        const int2 x1v = k == 0 ? make_int2(xa.x, xa.y) : k == 1 ? make_int2(xa.z, xa.w)
-                       : k == 2 ? make_int2(xb.x, xb.y) : make_int2(xb.z, xb.w);
-        const int nx = k == 0 ? xn.x : k == 1 ? xn.y : k == 2 ? xn.z : xn.w;
-        certify_px<NCH>(a, R, wres, k, sv, x1v, nx, apx, x1s, b, oy, blk, 4 * g + k, ox0 + k, cap, &s_nf);
+        for (int q = 0; q + 1 < NCH; ++q) apx[q] = k == 0 ? ap[q].x : ap[q].y;
+        const int32_t sv = k == 0 ? sab.x : sab.y;
+        const int2 x1v = k == 0 ? make_int2(xa.x, xa.y) : make_int2(xa.z, xa.w);
+        const int nx = k == 0 ? xn.x : xn.y;
+        certify_px<NCH>(a, R, wres, k, sv, x1v, nx, apx, x1s, b, oy, blk, 2 * g + k, ox0 + k, cap, &s_nf);
       }
     }
   } else {
