@@ -92,6 +92,36 @@ __device__ __forceinline__ void store_residues(long long v, int8_t* out, long lo
   }
 }
 
+// Symmetric residues of four integers |v| < 2^48 (magnitude + sign) packed into one word per
+// plane: |v| = h2 2^32 + h1 2^16 + h0 reduces to h2 (2^32 mod P) + h1 (2^16 mod P) + h0 < 2^26,
+// one 32-bit reduction (the compiler's multiply-high sequence) per value and modulus; P = 256
+// takes the low byte of the two's complement.
+template <int P>
+__device__ __forceinline__ uint32_t sres_byte(unsigned long long mag, bool neg) {
+  if constexpr (P == 256) {
+    return static_cast<uint32_t>(neg ? 0ull - mag : mag) & 0xffu;
+  } else {
+    constexpr uint32_t T16 = (1u << 16) % P, T32 = static_cast<uint32_t>((1ull << 32) % P);
+    const uint32_t h0 = static_cast<uint32_t>(mag) & 0xffffu, h1 = static_cast<uint32_t>(mag >> 16) & 0xffffu,
+                   h2 = static_cast<uint32_t>(mag >> 32);
+    const uint32_t r = (h2 * T32 + h1 * T16 + h0) % P;
+    int s = r > static_cast<uint32_t>((P - 1) / 2) ? static_cast<int>(r) - P : static_cast<int>(r);
+    if (neg) s = -s;  // P odd: the symmetric range is closed under negation
+    return static_cast<uint32_t>(s) & 0xffu;
+  }
+}
+template <int J = 0>
+__device__ __forceinline__ void store_residues4(const unsigned long long (&mag)[4], const bool (&neg)[4], int8_t* out,
+                                                long long plane) {
+  if constexpr (J < NMOD) {
+    constexpr int P = crt_mod(J);
+    const uint32_t w = sres_byte<P>(mag[0], neg[0]) | (sres_byte<P>(mag[1], neg[1]) << 8) |
+                       (sres_byte<P>(mag[2], neg[2]) << 16) | (sres_byte<P>(mag[3], neg[3]) << 24);
+    *reinterpret_cast<uint32_t*>(out + J * plane) = w;
+    store_residues4<J + 1>(mag, neg, out, plane);
+  }
+}
+
 // Launch-wide activation exponent: max|x| < 2^ex and max|x| * 2^(8-ex) <= 255.
 // Non-finite inputs or weights set their exponent to CRT_NONFINITE: no output is certified then,
 // and the chain reproduces the reference's NaN / Inf propagation.
@@ -232,31 +262,47 @@ __global__ void crt_x_kernel(const double* __restrict__ in, int B, int C, int H,
     if (xf && c < C && x < W) xf[((static_cast<long long>(b) * C + c) * H + y) * W + x] = static_cast<float>(v);  // exact
   }
   __syncthreads();
+  // one pixel x four channels per thread (blockDim 32 x 8 = 32 pixels x 8 channel groups): the
+  // four values' plane bytes go out as one 32-bit store per plane
   const long long plane = static_cast<long long>(B) * H * W * Cp;
-  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-    const int x = x0 + i, c = c0 + threadIdx.x;
-    int a = 0, inexact = 0;
-    if (x < W && c < Cp) {
-      const double v = tile[threadIdx.x][i];
-      const long long o = ((static_cast<long long>(b) * H + y) * W + x) * Cp + c;
-      const double xsc = v * pow2(bx - ex);  // exact (power-of-two scaling)
-      const long long xi = __double2ll_rn(xsc);
-      inexact = static_cast<double>(xi) != xsc ? 1 : 0;
-      store_residues(xi, out + o, plane);
-      a = static_cast<int>(ceil(fabs(v) * pow2(8 - ex)));
-      out[BOUND_PLANE * plane + o] = static_cast<int8_t>(static_cast<uint8_t>(a));
-      out[APPROX_PLANE * plane + o] = static_cast<int8_t>(rint(v * pow2(7 - eax)));  // |.| <= 127
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int cg = t & 7, px = t >> 3;
+  const int x = x0 + px, c = c0 + 4 * cg;
+  int a = 0, inexact = 0;
+  if (x < W && c < Cp) {
+    const long long o = ((static_cast<long long>(b) * H + y) * W + x) * Cp + c;
+    const double sx = pow2(bx - ex), sb = pow2(8 - ex), sa = pow2(7 - eax);
+    constexpr double MAGIC = 0x1.8p52;  // adding it rounds |v| < 2^51 to an integer (ties to even)
+    unsigned long long mag[4];
+    bool neg[4];
+    uint32_t bnd = 0, apx = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const double v = tile[4 * cg + e][px];
+      const double xsc = v * sx;              // exact (power-of-two scaling)
+      const double tr = xsc + MAGIC;          // rint(xsc) + MAGIC, exact
+      const long long xi = __double_as_longlong(tr) - __double_as_longlong(MAGIC);
+      inexact += (tr - MAGIC) != xsc ? 1 : 0;
+      neg[e] = xi < 0;
+      mag[e] = neg[e] ? 0ull - static_cast<unsigned long long>(xi) : static_cast<unsigned long long>(xi);
+      const int ab = static_cast<int>(ceil(fabs(v) * sb));
+      a += ab;
+      bnd |= static_cast<uint32_t>(ab & 0xff) << (8 * e);
+      apx |= (static_cast<uint32_t>(static_cast<int>(rint(v * sa))) & 0xffu) << (8 * e);  // |.| <= 127
     }
-    for (int s = 16; s; s >>= 1) {
-      a += __shfl_xor_sync(0xffffffffu, a, s);
-      inexact += __shfl_xor_sync(0xffffffffu, inexact, s);
-    }
-    if (threadIdx.x == 0 && x < W && inexact)
-      atomicAdd(&s1n[(static_cast<long long>(b) * H + y) * W + x], inexact);
-    // per chain chunk (a 32-channel tile lies in one chunk of chunk_ch = 64 or 128 channels)
-    if (threadIdx.x == 0 && x < W)
-      atomicAdd(&s1[(static_cast<long long>(c0 / chunk_ch) * B * H + static_cast<long long>(b) * H + y) * W + x], a);
+    int8_t* op = out + o;
+    store_residues4(mag, neg, op, plane);
+    *reinterpret_cast<uint32_t*>(op + BOUND_PLANE * plane) = bnd;
+    *reinterpret_cast<uint32_t*>(op + APPROX_PLANE * plane) = apx;
   }
+  for (int sft = 4; sft; sft >>= 1) {  // the 8 lanes of one pixel
+    a += __shfl_xor_sync(0xffffffffu, a, sft);
+    inexact += __shfl_xor_sync(0xffffffffu, inexact, sft);
+  }
+  if (cg == 0 && x < W && inexact) atomicAdd(&s1n[(static_cast<long long>(b) * H + y) * W + x], inexact);
+  // per chain chunk (a 32-channel tile lies in one chunk of chunk_ch channels)
+  if (cg == 0 && x < W)
+    atomicAdd(&s1[(static_cast<long long>(c0 / chunk_ch) * B * H + static_cast<long long>(b) * H + y) * W + x], a);
 }
 
 // x1[b][oy][ox] = sum over the k x k taps of s1: an upper bound (in 2^(ex-8) units) of the
