@@ -37,7 +37,6 @@
 #include <map>
 #include <memory>
 #include <string>
-#include <type_traits>
 
 #include "common.cuh"
 #include "crt.cuh"
@@ -1737,35 +1736,21 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
     const double* p0 = sR + pp[0];
     const double* p1 = sR + pp[1];
     const int nper = (nchunks + G::NCH - 1) / G::NCH;
-    // the chunk loop, unrolled over a period (every tap offset an immediate), for one or two
-    // live slots
-    auto run = [&](auto two_tag) {
-      constexpr bool TWO = decltype(two_tag)::value;
-      issue(0, 0);
-      for (int per = 0; per < nper; ++per) {
+    // the chunk loop, unrolled over a period (every tap offset an immediate); every thread of the
+    // block passes the same two barrier sites per chunk (the slot-count branch is inside)
+    issue(0, 0);
+    for (int per = 0; per < nper; ++per) {
 #pragma unroll
-        for (int jj = 0; jj < G::NCH; ++jj) {
-          const int ch = per * G::NCH + jj;
-          if (ch >= nchunks) break;
-          const int st = ch & 1;
-          if (ch + 1 < nchunks) issue(ch + 1, st ^ 1);
-          else cp_async_commit();
-          cp_async_wait<1>();
-          __syncthreads();
-          c6_dispatch<KS, DS, TWO>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], p0, p1, acc);
-          __syncthreads();
-        }
-      }
-    };
-    if (live[1]) run(std::integral_constant<bool, true>());
-    else if (live[0]) run(std::integral_constant<bool, false>());
-    else {  // no chain in this warp: still take part in the copies and barriers
-      issue(0, 0);
-      for (int ch = 0; ch < nchunks; ++ch) {
-        if (ch + 1 < nchunks) issue(ch + 1, (ch & 1) ^ 1);
+      for (int jj = 0; jj < G::NCH; ++jj) {
+        const int ch = per * G::NCH + jj;
+        if (ch >= nchunks) break;
+        const int st = ch & 1;
+        if (ch + 1 < nchunks) issue(ch + 1, st ^ 1);
         else cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
+        if (live[1]) c6_dispatch<KS, DS, true>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], p0, p1, acc);
+        else if (live[0]) c6_dispatch<KS, DS, false>(jj, &sW[st][0][tid][0], nullptr, p0, nullptr, acc);
         __syncthreads();
       }
     }
