@@ -549,7 +549,9 @@ __device__ __forceinline__ void crt_gemm_epilogue(const CrtGemmArgs& a, long lon
             const int rr = 4 * r4 + rsub;
             const uint32_t* t = tile + rr * 33 + 4 * cg;
             const uint32_t word = (t[0] & 0xffu) | ((t[1] & 0xffu) << 8) | ((t[2] & 0xffu) << 16) | (t[3] << 24);
-            *reinterpret_cast<uint32_t*>(base + static_cast<long long>(tl.m0 + q * 32 + rr) * plane_px) = word;
+            // streaming (evict-first) stores: the residue planes are read once, by the
+            // certification, and must not push the activation windows out of L2
+            __stcs(reinterpret_cast<unsigned int*>(base + static_cast<long long>(tl.m0 + q * 32 + rr) * plane_px), word);
           }
         } else if (px < a.OW) {
           const long long row0 = static_cast<long long>(tl.oy) * a.OW + px;
@@ -564,7 +566,8 @@ __device__ __forceinline__ void crt_gemm_epilogue(const CrtGemmArgs& a, long lon
                                : a.approx + (static_cast<long long>(tl.plane - BOUND_PLANE - 1) * a.B + tl.b) * a.Mp * plane_px + row0;
 #pragma unroll 8
             for (int rr = 0; rr < 32; ++rr)
-              dst[static_cast<long long>(tl.m0 + q * 32 + rr) * plane_px] = static_cast<int32_t>(tile[rr * 33 + lane]);
+              __stcs(reinterpret_cast<int*>(dst + static_cast<long long>(tl.m0 + q * 32 + rr) * plane_px),
+                     static_cast<int>(tile[rr * 33 + lane]));
           }
         }
         __syncwarp();
