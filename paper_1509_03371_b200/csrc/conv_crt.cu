@@ -1711,19 +1711,21 @@ struct C6Geo {
 template <int KS, int DS>
 constexpr size_t c6_smem_bytes() {
   using G = C6Geo<KS, DS>;
-  return sizeof(float) * 2 * C3_SLOTS * C3_THREADS * (G::TK + 4) + sizeof(double) * G::NR * G::RWP +
+  return sizeof(float) * 2 * C3_SLOTS * C3_THREADS * G::TK + sizeof(double) * G::NR * G::RWP +
          sizeof(uint32_t) * C3_SORT_CAP;
 }
 // one chunk (position J in the period): TK taps of both slots (TWO) or slot 0 only
+// Weight runs are 32-byte rows with their two 16-byte halves swapped on every other group of
+// four rows (sw = (row >> 2) & 1): the LDS.128 of a quarter warp then covers all 32 banks.
 template <int KS, int DS, int J, bool TWO>
-__device__ __forceinline__ void c6_chunk(const float* __restrict__ w0, const float* __restrict__ w1, const double* p0,
-                                         const double* p1, double (&acc)[C3_SLOTS]) {
+__device__ __forceinline__ void c6_chunk(const float* __restrict__ w0, const float* __restrict__ w1, int sw,
+                                         const double* p0, const double* p1, double (&acc)[C3_SLOTS]) {
   using G = C6Geo<KS, DS>;
 #pragma unroll
   for (int v = 0; v < G::TK / 4; ++v) {
-    const float4 wa = reinterpret_cast<const float4*>(w0)[v];
+    const float4 wa = reinterpret_cast<const float4*>(w0)[v ^ sw];
     float4 wb;
-    if constexpr (TWO) wb = reinterpret_cast<const float4*>(w1)[v];
+    if constexpr (TWO) wb = reinterpret_cast<const float4*>(w1)[v ^ sw];
     const float wav[4] = {wa.x, wa.y, wa.z, wa.w};
     float wbv[4];
     if constexpr (TWO) {
@@ -1742,16 +1744,19 @@ __device__ __forceinline__ void c6_chunk(const float* __restrict__ w0, const flo
   }
 }
 template <int KS, int DS, bool TWO, int J = 0>
-__device__ __forceinline__ void c6_dispatch(int j, const float* w0, const float* w1, const double* p0, const double* p1,
-                                            double (&acc)[C3_SLOTS]) {
+__device__ __forceinline__ void c6_dispatch(int j, const float* w0, const float* w1, int sw, const double* p0,
+                                            const double* p1, double (&acc)[C3_SLOTS]) {
   if constexpr (J < C6Geo<KS, DS>::NCH) {
-    if (j == J) c6_chunk<KS, DS, J, TWO>(w0, w1, p0, p1, acc);
-    else c6_dispatch<KS, DS, TWO, J + 1>(j, w0, w1, p0, p1, acc);
+    if (j == J) c6_chunk<KS, DS, J, TWO>(w0, w1, sw, p0, p1, acc);
+    else c6_dispatch<KS, DS, TWO, J + 1>(j, w0, w1, sw, p0, p1, acc);
   }
 }
 
+#ifndef CRT_C6_MINB
+#define CRT_C6_MINB 7  // 72 registers, 28.5 KB of shared memory: 7 blocks (28 warps) per SM
+#endif
 template <int KS, int DS>
-__global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
+__global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
     crt_chain6_kernel(const CrtFinishArgs a) {
   using G = C6Geo<KS, DS>;
   constexpr int TK = G::TK, NR = G::NR, RWP = G::RWP, C6_PX = G::PX;
@@ -1759,8 +1764,8 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
   constexpr uint32_t PXM = (1u << PXB) - 1;
   constexpr int SEGS = C6_PX / FIN_PX;
   extern __shared__ __align__(16) unsigned char c6_smem[];
-  auto sW = reinterpret_cast<float(*)[C3_SLOTS][C3_THREADS][TK + 4]>(c6_smem);
-  double* sR = reinterpret_cast<double*>(c6_smem + sizeof(float) * 2 * C3_SLOTS * C3_THREADS * (TK + 4));
+  auto sW = reinterpret_cast<float(*)[C3_SLOTS][C3_THREADS][TK]>(c6_smem);
+  double* sR = reinterpret_cast<double*>(c6_smem + sizeof(float) * 2 * C3_SLOTS * C3_THREADS * TK);
   uint32_t* s_list = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sR) + sizeof(double) * NR * RWP);
   __shared__ int s_pre[SEGS + 1];
   __shared__ int s_cnt[C6_PX + 1];
@@ -1840,7 +1845,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
     // this thread's cooperative weight copies, fixed for the pass: global float offset of the
     // 16-byte piece (chain row m, piece pc) and its shared-memory byte offset within a stage
     constexpr int PIECES = TK / 4, NCOPY = C3_SLOTS * PIECES;
-    constexpr uint32_t STAGE_BYTES = sizeof(float) * C3_SLOTS * C3_THREADS * (TK + 4);
+    constexpr uint32_t STAGE_BYTES = sizeof(float) * C3_SLOTS * C3_THREADS * TK;
     int woff[NCOPY];
     uint32_t wsm[NCOPY];
     bool wok[NCOPY];
@@ -1852,7 +1857,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
       const int m = s_m[c][t];
       wok[e] = m >= 0;
       woff[e] = (m >= 0 ? m : 0) * a.K + 4 * pc;  // < 2^31: M * K <= 2^31 checked at launch
-      wsm[e] = smem_u32(&sW[0][c][t][4 * pc]);
+      wsm[e] = smem_u32(&sW[0][c][t][4 * (pc ^ ((t >> 2) & 1))]);
     }
     auto issue = [&](int ch, int stage) {
       const int kc = ch * TK;
@@ -1890,8 +1895,9 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
         else cp_async_commit();
         cp_async_wait<1>();
         __syncthreads();
-        if (live[1]) c6_dispatch<KS, DS, true>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], p0, p1, acc);
-        else if (live[0]) c6_dispatch<KS, DS, false>(jj, &sW[st][0][tid][0], nullptr, p0, nullptr, acc);
+        const int sw = (tid >> 2) & 1;
+        if (live[1]) c6_dispatch<KS, DS, true>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], sw, p0, p1, acc);
+        else if (live[0]) c6_dispatch<KS, DS, false>(jj, &sW[st][0][tid][0], nullptr, sw, p0, nullptr, acc);
         __syncthreads();
       }
     }
