@@ -1697,6 +1697,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C3_MINB)
 // tap's (ring slot, kx*DS) offset inside an unrolled period of chunks is an immediate, so a chain
 // step is still one LDS + one DFMA + one F2F. Weights are staged exactly as in v3.
 __host__ __device__ constexpr int c6_gcd(int a, int b) { return b == 0 ? a : c6_gcd(b, a % b); }
+constexpr int C6_SORT_CAP = 896;  // chains a block sorts by pixel (8 blocks per SM fit with this list)
 template <int KS, int DS>
 struct C6Geo {
   static constexpr int TK = 8;                                   // taps per chunk (weight runs of 32 B)
@@ -1706,13 +1707,13 @@ struct C6Geo {
   static constexpr int NCH = PT / TK;                            // chunks per period
   static constexpr int PX = 4 * FIN_PX;                          // pixels per block
   static constexpr int RWIN = PX + (KS - 1) * DS;                // window (f64) per kernel row
-  static constexpr int RWP = RWIN + 2;                           // padded pitch (f64)
+  static constexpr int RWP = RWIN;                               // window pitch (f64)
 };
 template <int KS, int DS>
 constexpr size_t c6_smem_bytes() {
   using G = C6Geo<KS, DS>;
   return sizeof(float) * 2 * C3_SLOTS * C3_THREADS * G::TK + sizeof(double) * G::NR * G::RWP +
-         sizeof(uint32_t) * C3_SORT_CAP;
+         sizeof(uint32_t) * C6_SORT_CAP;
 }
 // one chunk (position J in the period): TK taps of both slots (TWO) or slot 0 only
 // Weight runs are 32-byte rows with their two 16-byte halves swapped on every other group of
@@ -1753,7 +1754,7 @@ __device__ __forceinline__ void c6_dispatch(int j, const float* w0, const float*
 }
 
 #ifndef CRT_C6_MINB
-#define CRT_C6_MINB 7  // 72 registers, 28.5 KB of shared memory: 7 blocks (28 warps) per SM
+#define CRT_C6_MINB 7  // 72 registers, 7 blocks (28 warps) per SM (8 blocks at 64 registers: 0.5 ms slower)
 #endif
 template <int KS, int DS>
 __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
@@ -1795,7 +1796,7 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
     const uint32_t e = a.fail_list[(sb0 + sg) * a.cap + (f - s_pre[sg])];
     return ((e >> 5) << PXB) | static_cast<uint32_t>(sg * FIN_PX + static_cast<int>(e & 31));
   };
-  const bool sorted = nf <= C3_SORT_CAP;
+  const bool sorted = nf <= C6_SORT_CAP;
   if (sorted) {  // counting sort by pixel
     for (int i = tid; i <= C6_PX; i += C3_THREADS) s_cnt[i] = 0;
     __syncthreads();
