@@ -1251,14 +1251,19 @@ __global__ void __launch_bounds__(FIN_THREADS, CRT_CERT2_MINB) crt_certify2_kern
 // chunks of the block's 32-pixel slab -- the 12 residue planes, the bound and the chunk sums,
 // 36 KB per chunk at NCH = 6 -- into a two-stage ring with one 2D tensor copy per plane, and the
 // 8 consumer warps read them from shared memory (4 pixels of one row m per thread).
-constexpr int CT3_R = 32, CT3_CONSUMERS = 256, CT3_THREADS = CT3_CONSUMERS + 32;
+#ifndef CRT_CT3_R
+#define CRT_CT3_R 32   // rows of f_out per ring stage (16 rows x 4 stages measured 1.1 ms slower)
+#define CRT_CT3_ST 2   // ring stages
+#endif
+constexpr int CT3_R = CRT_CT3_R, CT3_ST = CRT_CT3_ST, CT3_CONSUMERS = 256, CT3_THREADS = CT3_CONSUMERS + 32;
+constexpr int CT3_PPT = CT3_R / 8;  // pixels per consumer thread (256 threads over R rows x 32 pixels)
 template <int NCH>
 __host__ __device__ constexpr size_t ct3_stage_bytes() {
   return static_cast<size_t>(CT3_R) * FIN_PX * (NMOD + 4 + 4 * (NCH > 1 ? NCH - 1 : 0));
 }
 template <int NCH>
 __host__ __device__ constexpr size_t ct3_smem_bytes() {
-  return 1024 + 2 * ct3_stage_bytes<NCH>();
+  return 1024 + CT3_ST * ct3_stage_bytes<NCH>();
 }
 #ifndef CRT_CERT3_MINB
 #define CRT_CERT3_MINB 3  // 72 registers (36 B of spills), 3 blocks per SM: 15.3 vs 16.3 ms at 2
@@ -1272,7 +1277,7 @@ __global__ void __launch_bounds__(CT3_THREADS, CRT_CERT3_MINB)
   constexpr unsigned STAGE = static_cast<unsigned>(ct3_stage_bytes<NCH>());
   extern __shared__ uint8_t ct3_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(ct3_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-  __shared__ uint64_t full[2], empty[2];
+  __shared__ uint64_t full[CT3_ST], empty[CT3_ST];
   __shared__ int s_nf;
   __shared__ int2 s_x1[FIN_PX];
   __shared__ int s_xn[FIN_PX];
@@ -1285,7 +1290,7 @@ __global__ void __launch_bounds__(CT3_THREADS, CRT_CERT3_MINB)
   const long long xrow = (static_cast<long long>(b) * a.OH + oy) * a.OW;
   if (tid == 0) {
     s_nf = 0;
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < CT3_ST; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CT3_CONSUMERS / 32);
     }
@@ -1302,8 +1307,8 @@ __global__ void __launch_bounds__(CT3_THREADS, CRT_CERT3_MINB)
   if (warp == 0) {
     if (lane == 0) {
       for (int c = 0; c < nck; ++c) {
-        const int s = c & 1;
-        if (c >= 2) mbar_wait(&empty[s], static_cast<unsigned>(((c >> 1) - 1) & 1));
+        const int s = c % CT3_ST;
+        if (c >= CT3_ST) mbar_wait(&empty[s], static_cast<unsigned>(((c / CT3_ST) - 1) & 1));
         mbar_expect_tx(&full[s], STAGE);
         uint8_t* st = smem + s * STAGE;
         const int row0 = b * a.Mp + c * CT3_R;
@@ -1322,28 +1327,34 @@ __global__ void __launch_bounds__(CT3_THREADS, CRT_CERT3_MINB)
     const double xmaxv = __longlong_as_double(static_cast<long long>(*a.xmax_bits));
     const int cap = min(a.cap, FIN_CAP);
     const int t = tid - 32;
-    const int r = t >> 3, g = t & 7;  // row in the chunk, 4-pixel group
+    constexpr int TPR = 32 / CT3_PPT;  // threads per row
+    const int r = t / TPR, g = t % TPR;  // row in the chunk, pixel group
     for (int c = 0; c < nck; ++c) {
-      const int s = c & 1;
-      mbar_wait(&full[s], static_cast<unsigned>((c >> 1) & 1));
+      const int s = c % CT3_ST;
+      mbar_wait(&full[s], static_cast<unsigned>((c / CT3_ST) & 1));
       const int m = c * CT3_R + r;
-      if (m < a.M && px0 + 4 * g < a.OW) {
+      const int p0 = CT3_PPT * g;
+      if (m < a.M && px0 + p0 < a.OW) {
         const uint8_t* st = smem + s * STAGE;
         uint32_t wres[NMOD];
 #pragma unroll
-        for (int j = 0; j < NMOD; ++j) wres[j] = *reinterpret_cast<const uint32_t*>(st + j * RES_B + r * FIN_PX + 4 * g);
+        for (int j = 0; j < NMOD; ++j) {
+          const uint8_t* src = st + j * RES_B + r * FIN_PX + p0;
+          if constexpr (CT3_PPT == 4) wres[j] = *reinterpret_cast<const uint32_t*>(src);
+          else wres[j] = *reinterpret_cast<const unsigned short*>(src);
+        }
         const CertRow R = make_cert_row<NCH>(a, m, ex, eax, sx, xmaxv);
-        const int32_t* sab = reinterpret_cast<const int32_t*>(st + NMOD * RES_B) + r * FIN_PX + 4 * g;
-        const int32_t* apb = reinterpret_cast<const int32_t*>(st + NMOD * RES_B + I32_B) + r * FIN_PX + 4 * g;
+        const int32_t* sab = reinterpret_cast<const int32_t*>(st + NMOD * RES_B) + r * FIN_PX + p0;
+        const int32_t* apb = reinterpret_cast<const int32_t*>(st + NMOD * RES_B + I32_B) + r * FIN_PX + p0;
 #pragma unroll 1
-        for (int k = 0; k < 4; ++k) {
-          const int ox = px0 + 4 * g + k;
+        for (int k = 0; k < CT3_PPT; ++k) {
+          const int ox = px0 + p0 + k;
           if (ox >= a.OW) break;
           int32_t apx[NCH > 1 ? NCH - 1 : 1];
 #pragma unroll
           for (int q = 0; q < NQ; ++q) apx[q] = apb[q * CT3_R * FIN_PX + k];
-          certify_px<NCH>(a, R, wres, k, sab[k], s_x1[4 * g + k], s_xn[4 * g + k], apx, x1s, b, oy, blk, 4 * g + k, ox,
-                          cap, &s_nf);
+          certify_px<NCH>(a, R, wres, k, sab[k], s_x1[p0 + k], s_xn[p0 + k], apx, x1s, b, oy, blk, p0 + k, ox, cap,
+                          &s_nf);
         }
       }
       release_stage(&empty[s], lane);
