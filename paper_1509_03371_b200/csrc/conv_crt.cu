@@ -7,7 +7,7 @@
 //     launch (|Wi| <= 2^bw, |Xi| <= 2^bx, bw + bx chosen so K * 2^(bw+bx) < Mprod / 2);
 //  2. the exact integer P = sum Wi*Xi is computed modulo 12 pairwise-coprime moduli <= 256 --
 //     each one an s8 x s8 -> s32 implicit-GEMM conv on tcgen05 (kind::i8, exact in any order)
-//     -- and reconstructed by CRT (Ozaki scheme II) from three exact 37-bit limb sums;
+//     -- and reconstructed by CRT (Ozaki scheme II) in fractional form (certify_px);
 //  3. a rigorous interval [V - E, V + E] holds the reference's acc. E = fixed-point truncation
 //     + the chain's own rounding. The operands are floats, so a tap's fixed-point value is exact
 //     unless the operand lies far below its row / launch maximum (bw = 40, bx = 39 for sk.net's
