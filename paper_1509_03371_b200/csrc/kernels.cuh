@@ -32,6 +32,11 @@ void tile_conv_weights(const float* w_f32_dev, int M, int K, double* tiled, cuda
 // out_f64 = conv blob, out_relu_f64 = relu(conv) (fused relu_forward), out_f32 = conv as f32.
 void conv_exact(const double* in, const double* w_tiled, const float* bias, const ConvShape& sh,
                 double* out_f64, double* out_relu_f64, float* out_f32, cudaStream_t st);
+// The same for 1x1 convs with f_out <= 8 (two-class heads), from the f32 weights [M][C]: one
+// thread per pixel, the f_out chains in registers (conv_exact.cu conv_narrow_kernel).
+bool conv_narrow_eligible(const ConvShape& sh);
+void conv_narrow(const double* in, const float* w_f32, const float* bias, const ConvShape& sh, double* out_f64,
+                 double* out_relu_f64, float* out_f32, cudaStream_t st);
 
 // TMA-fed variant (conv_tma.cu) used by conv_exact for stride-1 layers with 16-byte row
 // pitches (every net blob); same arithmetic, same results.

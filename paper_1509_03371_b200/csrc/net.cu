@@ -402,6 +402,9 @@ int run_layers(graft_net& n, bool mode_process) {
                           out_relu, n.crt_scratch, n.stream, n.timed && fan_in >= n.crt_min_k))
               conv_exact(in.buf.as<double>(), l.w_tiled.as<double>(), l.bias_dev.as<float>(), sh, out, out_relu,
                          nullptr, n.stream);
+          } else if (conv_narrow_eligible(sh)) {
+            conv_narrow(in.buf.as<double>(), l.w_f32.as<float>(), l.bias_dev.as<float>(), sh, out, out_relu, nullptr,
+                        n.stream);
           } else {
             conv_exact(in.buf.as<double>(), l.w_tiled.as<double>(), l.bias_dev.as<float>(), sh,
                        out, out_relu, nullptr, n.stream);
