@@ -922,22 +922,29 @@ __global__ void __launch_bounds__(192, 1)
         bool narrow;
         plane_range(tl.plane, dp, s0, s1, kk0, kk1, narrow, c32);
         const int px = tl.ox0 + static_cast<int>(rank) * (WIDE ? BN : BN / 2);
-        for (int ky = 0; ky < a.k; ++ky) {
+        // a narrow (32-byte) chunk-sum plane packs two kernel rows per stage: the same bytes and
+        // MMA work per stage as a full plane, half the stages (and their barrier round trips)
+        const int rpk = (narrow && !WIDE) ? 2 : 1;
+        for (int ky = 0; ky < a.k; ky += rpk) {
+          const int nr = min(rpk, a.k - ky);
           for (int sc = s0; sc < s1; ++sc, ++g) {
             const int s = static_cast<int>(g % STAGES);
             if (g >= STAGES) mbar_wait(&empty[s], static_cast<unsigned>(((g / STAGES) - 1) & 1));
             const unsigned rowb = narrow ? 32u : static_cast<unsigned>(KB);
-            if (leader) mbar_expect_tx(&full[s], 2 * (a.k * 128 * rowb + brows * rowb));
+            if (leader) mbar_expect_tx(&full[s], 2 * nr * (a.k * 128 * rowb + brows * rowb));
             const uint32_t fb = mapa_rank(&full[s], 0);
             const int coff = narrow ? c32 : sc * KB;
-            tma2_load_4d(sB + s * B_STAGE, narrow ? &tmB32 : &tmB, coff, px, tl.oy + ky * a.d, dp * a.B + tl.b, fb);
-            if (WIDE)  // rows 256 .. 256 + (k-1) d of the window, right behind the first box
-              tma2_load_4d(sB + s * B_STAGE + 256 * rowb, narrow ? &tmB322 : &tmB2, coff, px + 256, tl.oy + ky * a.d,
+            for (int r = 0; r < nr; ++r) {
+              tma2_load_4d(sB + s * B_STAGE + r * 8192, narrow ? &tmB32 : &tmB, coff, px, tl.oy + (ky + r) * a.d,
                            dp * a.B + tl.b, fb);
-            for (int kx = 0; kx < a.k; ++kx) {
-              const int tap = ky * a.k + kx;
-              tma2_load_2d(sA + s * A_STAGE + kx * (narrow ? N32 : A_BYTES), narrow ? &tmA32 : &tmA,
-                           tap * a.Cp + coff, dp * a.Mp + tl.m0, fb);
+              if (WIDE)  // rows 256 .. 256 + (k-1) d of the window, right behind the first box
+                tma2_load_4d(sB + s * B_STAGE + 256 * rowb, narrow ? &tmB322 : &tmB2, coff, px + 256,
+                             tl.oy + ky * a.d, dp * a.B + tl.b, fb);
+              for (int kx = 0; kx < a.k; ++kx) {
+                const int tap = (ky + r) * a.k + kx;
+                tma2_load_2d(sA + s * A_STAGE + (r * a.k + kx) * (narrow ? N32 : A_BYTES), narrow ? &tmA32 : &tmA,
+                             tap * a.Cp + coff, dp * a.Mp + tl.m0, fb);
+              }
             }
           }
         }
@@ -961,19 +968,22 @@ __global__ void __launch_bounds__(192, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t acc = tmem + static_cast<uint32_t>(buf * BN);
         uint32_t accumulate = 0;
-        for (int ky = 0; ky < a.k; ++ky) {
+        const int rpk = (narrow && !WIDE) ? 2 : 1;
+        for (int ky = 0; ky < a.k; ky += rpk) {
+          const int nr = min(rpk, a.k - ky);
           for (int sc = s0; sc < s1; ++sc, ++g) {
             const int s = static_cast<int>(g % STAGES);
             mbar_wait(&full[s], static_cast<unsigned>((g / STAGES) & 1));
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             if (narrow) {
-              for (int kx = 0; kx < a.k; ++kx) {
-                const uint64_t da = da32 + static_cast<uint64_t>((s * A_STAGE + kx * N32) >> 4);
-                const uint64_t db = db32 + static_cast<uint64_t>((s * B_STAGE + kx * a.d * 32) >> 4);
-                mma2_i8(acc, da, db, idesc, accumulate);
-                if (WIDE) mma2_i8(acc + BN, da, db + static_cast<uint64_t>((128 * 32) >> 4), idesc, accumulate);
-                accumulate = 1;
-              }
+              for (int r = 0; r < nr; ++r)
+                for (int kx = 0; kx < a.k; ++kx) {
+                  const uint64_t da = da32 + static_cast<uint64_t>((s * A_STAGE + (r * a.k + kx) * N32) >> 4);
+                  const uint64_t db = db32 + static_cast<uint64_t>((s * B_STAGE + r * 8192 + kx * a.d * 32) >> 4);
+                  mma2_i8(acc, da, db, idesc, accumulate);
+                  if (WIDE) mma2_i8(acc + BN, da, db + static_cast<uint64_t>((128 * 32) >> 4), idesc, accumulate);
+                  accumulate = 1;
+                }
             } else {
               const int nm = min(kk1, sc == a.cchunks - 1 ? a.last_mmas : MMAS);
               for (int kx = 0; kx < a.k; ++kx) {
