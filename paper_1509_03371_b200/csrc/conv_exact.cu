@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(256) conv_narrow_kernel(const double* __restri
     double acc[MM];
 #pragma unroll
     for (int m = 0; m < MM; ++m) acc[m] = 0.0;
-#pragma unroll 4
+#pragma unroll 16
     for (int c = 0; c < a.C; ++c) {
       const double v = __ldg(x + c * HW);
 #pragma unroll
