@@ -72,6 +72,8 @@ struct DeviceContext {
   size_t scratch_bytes = 0;
   void* scratch2 = nullptr;
   size_t scratch2_bytes = 0;
+  void* gemm_ops[2] = {nullptr, nullptr};  // widened f64 operands of the gemm API (grow-only)
+  size_t gemm_ops_bytes[2] = {0, 0};
 };
 
 DeviceContext& ctx();                      // context of the calling thread's current device
