@@ -2568,6 +2568,14 @@ bool conv_crt(const double* in, const CrtWeights& cw, const float* w_f32, const 
       chain6(crt_chain6_kernel<10, 8>, c6_smem_bytes<10, 8>());
     } else if (c6_ok && sh.k == 8 && sh.d == 8) {
       chain6(crt_chain6_kernel<8, 8>, c6_smem_bytes<8, 8>());
+    } else if (c6_ok && sh.k == 3 && sh.d == 4) {  // sk.net conv3 (int8 when tuned)
+      chain6(crt_chain6_kernel<3, 4>, c6_smem_bytes<3, 4>());
+    } else if (c6_ok && sh.k == 3 && sh.d == 1) {  // u.net's 3x3 convs
+      chain6(crt_chain6_kernel<3, 1>, c6_smem_bytes<3, 1>());
+    } else if (c6_ok && sh.k == 4 && sh.d == 2) {  // usk.net conv4
+      chain6(crt_chain6_kernel<4, 2>, c6_smem_bytes<4, 2>());
+    } else if (c6_ok && sh.k == 4 && sh.d == 4) {  // usk.net conv5
+      chain6(crt_chain6_kernel<4, 4>, c6_smem_bytes<4, 4>());
     } else if (chain_kind == 3 || chain_kind == 6) {
       const int nsx = (sh.OW + FIN_PX - 1) / FIN_PX;
       // pixels per block: 128 (4 certify segments; bench image: chain 46 ms vs 49 at 64 px,

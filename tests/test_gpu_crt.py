@@ -101,7 +101,9 @@ def test_crt_chain_kernels(monkeypatch, chain):
                 assert nf == got.numel()
 
 
-@pytest.mark.parametrize("case", [(1, 192, 80, 100, 256, 10, 8, "pool"), (1, 128, 66, 93, 130, 8, 8, "signed")])
+@pytest.mark.parametrize("case", [(1, 192, 80, 100, 256, 10, 8, "pool"), (1, 128, 66, 93, 130, 8, 8, "signed"),
+                                  (1, 128, 30, 170, 192, 3, 4, "pool"), (2, 64, 20, 140, 100, 3, 1, "signed"),
+                                  (1, 128, 24, 150, 128, 4, 2, "pool"), (1, 128, 30, 150, 128, 4, 4, "signed")])
 def test_crt_chain6_kernel_ring(monkeypatch, case):
     """The kernel-row ring chain kernel (v6: instantiated for k, d = 10, 8 and 8, 8) on real
     failures and on every output forced through it, against v3 and the DMMA conv, both bit for
