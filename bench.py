@@ -487,6 +487,13 @@ def run_ours(args):
         cms = (ctypes.c_double * 4)()
         cl = ctypes.c_longlong()
         _lib.check(_lib.lib().graft_net_crt_stats(net, cms, ctypes.byref(cl)))
+        # OPT_CRT_FALLBACKS is the LAST int8 conv's count; the tuned ip2 may follow ip1 on the int8
+        # path, so one untimed run with the tuning off (ip2 on DMMA) reads ip1's own count
+        tune_k = proc.net.get_option(_lib.OPT_CRT_TUNE_MIN_K)
+        proc.net.set_option(_lib.OPT_CRT_TUNE_MIN_K, 0)
+        proc.run(img_d, w, args.v, lab_d, prob_d, mem=_lib.MEM_DEVICE)
+        ip1_fallbacks = proc.net.get_option(_lib.OPT_CRT_FALLBACKS)
+        proc.net.set_option(_lib.OPT_CRT_TUNE_MIN_K, tune_k)
         if cl.value > 0:
             # ip1 on the int8 path: crt_gemm2_kernel dominates. Algorithmic int8 ops = 2*M*N*K with
             # the layer's own K times (the residue planes + the bound plane + the chain-chunk sum
@@ -529,7 +536,7 @@ def run_ours(args):
                 "ip1_share_of_step": ip1_ms / all_ms if all_ms else None,
                 "ip1_breakdown_ms_per_step": {"activation_prep": cms[0] / args.steps, "residue_gemms": cms[1] / args.steps,
                                               "crt_certify": cms[2] / args.steps, "exact_chain_fallback": cms[3] / args.steps},
-                "ip1_chain_fallbacks_per_launch": proc.net.get_option(_lib.OPT_CRT_FALLBACKS),
+                "ip1_chain_fallbacks_per_launch": ip1_fallbacks,
                 "ip1_outputs_per_launch": 1024 * wi * wi,
                 "fp64_peak_tflops": peak_sustained,
                 "whole_net_fp64_equiv_tflops": fl["total"] * n_tiles * args.steps / (total_ms * 1e-3) / 1e12,
