@@ -97,24 +97,21 @@ __device__ __forceinline__ void store_residues(long long v, int8_t* out, long lo
   }
 }
 
-// Symmetric residues of four integers |v| < 2^48 (magnitude + sign) packed into one word per
-// plane: |v| = h2 2^32 + h1 2^16 + h0 reduces to h2 (2^32 mod P) + h1 (2^16 mod P) + h0 < 2^26,
-// one 32-bit reduction (the compiler's multiply-high sequence) per value and modulus; P = 256
+// Symmetric residues of four integers |v| < 2^47 (magnitude + sign) packed into one word per
+// plane: one 24-bit limb fold and one exact multiply-high division per value and modulus; P = 256
 // takes the low byte of the two's complement.
 template <int P>
 __device__ __forceinline__ uint32_t sres_byte(unsigned long long mag, bool neg) {
   if constexpr (P == 256) {
     return static_cast<uint32_t>(neg ? 0ull - mag : mag) & 0xffu;
   } else {
-    constexpr uint32_t T16 = (1u << 16) % P, T32 = static_cast<uint32_t>((1ull << 32) % P);
-    const uint32_t h0 = static_cast<uint32_t>(mag) & 0xffffu, h1 = static_cast<uint32_t>(mag >> 16) & 0xffffu,
-                   h2 = static_cast<uint32_t>(mag >> 32);
-    // v < 2^25; floor(v / P) = umulhi(v, ceil(2^39 / P)) >> 7 exactly for every odd modulus
-    // here (all 217 <= P <= 255) and v < 2^26 (checked exhaustively on the host), one
-    // multiply-high fewer than the compiler's general 32-bit sequence
+    // |v| = hi 2^24 + lo with hi < 2^23 (|v| < 2^47: bx <= 47 and max|x| 2^(8-ex) <= 255), so
+    // hi (2^24 mod P) + lo < 2^31.01, and floor(. / P) = umulhi(., ceil(2^39 / P)) >> 7 exactly
+    // there for every odd modulus 217..255 (checked exhaustively on the host)
     static_assert(P > 128 && P < 256, "magic division assumes 2^7 < P < 2^8");
+    constexpr uint32_t T24 = (1u << 24) % P;
     constexpr uint32_t MAGIC = static_cast<uint32_t>(((1ull << 39) + P - 1) / P);
-    const uint32_t v = h2 * T32 + h1 * T16 + h0;
+    const uint32_t v = static_cast<uint32_t>(mag >> 24) * T24 + (static_cast<uint32_t>(mag) & 0xffffffu);
     const uint32_t r = v - (__umulhi(v, MAGIC) >> 7) * P;
     int s = r > static_cast<uint32_t>((P - 1) / 2) ? static_cast<int>(r) - P : static_cast<int>(r);
     if (neg) s = -s;  // P odd: the symmetric range is closed under negation
