@@ -1770,52 +1770,53 @@ struct C6Geo {
   static constexpr int RWIN = PX + (KS - 1) * DS;                // window (f64) per kernel row
   static constexpr int RWP = RWIN;                               // window pitch (f64)
 };
+#ifndef CRT_C6_SLOTS
+#define CRT_C6_SLOTS 2  // chains per thread (3 measured 1.3 ms slower: 6 blocks per SM instead of 7)
+#endif
+constexpr int C6_SLOTS = CRT_C6_SLOTS;
 template <int KS, int DS>
 constexpr size_t c6_smem_bytes() {
   using G = C6Geo<KS, DS>;
-  return sizeof(float) * 2 * C3_SLOTS * C3_THREADS * G::TK + sizeof(double) * G::NR * G::RWP +
+  return sizeof(float) * 2 * C6_SLOTS * C3_THREADS * G::TK + sizeof(double) * G::NR * G::RWP +
          sizeof(uint32_t) * C6_SORT_CAP;
 }
 // one chunk (position J in the period): TK taps of both slots (TWO) or slot 0 only
 // Weight runs are 32-byte rows with their two 16-byte halves swapped on every other group of
 // four rows (sw = (row >> 2) & 1): the LDS.128 of a quarter warp then covers all 32 banks.
-template <int KS, int DS, int J, bool TWO>
-__device__ __forceinline__ void c6_chunk(const float* __restrict__ w0, const float* __restrict__ w1, int sw,
-                                         const double* p0, const double* p1, double (&acc)[C3_SLOTS]) {
+template <int KS, int DS, int J, int NL>
+__device__ __forceinline__ void c6_chunk(const float* const (&w)[C6_SLOTS], int sw, const double* const (&pz)[C6_SLOTS],
+                                         double (&acc)[C6_SLOTS]) {
   using G = C6Geo<KS, DS>;
 #pragma unroll
   for (int v = 0; v < G::TK / 4; ++v) {
-    const float4 wa = reinterpret_cast<const float4*>(w0)[v ^ sw];
-    float4 wb;
-    if constexpr (TWO) wb = reinterpret_cast<const float4*>(w1)[v ^ sw];
-    const float wav[4] = {wa.x, wa.y, wa.z, wa.w};
-    float wbv[4];
-    if constexpr (TWO) {
-      wbv[0] = wb.x;
-      wbv[1] = wb.y;
-      wbv[2] = wb.z;
-      wbv[3] = wb.w;
+    float wv[NL][4];
+#pragma unroll
+    for (int c = 0; c < NL; ++c) {
+      const float4 q = reinterpret_cast<const float4*>(w[c])[v ^ sw];
+      wv[c][0] = q.x;
+      wv[c][1] = q.y;
+      wv[c][2] = q.z;
+      wv[c][3] = q.w;
     }
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const int u = J * G::TK + 4 * v + e;                     // tap within the period (constant)
+      const int u = J * G::TK + 4 * v + e;  // tap within the period (constant)
       const int off = ((u / KS) % G::NR) * G::RWP + (u % KS) * DS;
-      acc[0] = fma(static_cast<double>(wav[e]), p0[off], acc[0]);
-      if constexpr (TWO) acc[1] = fma(static_cast<double>(wbv[e]), p1[off], acc[1]);
+#pragma unroll
+      for (int c = 0; c < NL; ++c) acc[c] = fma(static_cast<double>(wv[c][e]), pz[c][off], acc[c]);
     }
   }
 }
-template <int KS, int DS, bool TWO, int J = 0>
-__device__ __forceinline__ void c6_dispatch(int j, const float* w0, const float* w1, int sw, const double* p0,
-                                            const double* p1, double (&acc)[C3_SLOTS]) {
+template <int KS, int DS, int NL, int J = 0>
+__device__ __forceinline__ void c6_dispatch(int j, const float* const (&w)[C6_SLOTS], int sw,
+                                            const double* const (&pz)[C6_SLOTS], double (&acc)[C6_SLOTS]) {
   if constexpr (J < C6Geo<KS, DS>::NCH) {
-    if (j == J) c6_chunk<KS, DS, J, TWO>(w0, w1, sw, p0, p1, acc);
-    else c6_dispatch<KS, DS, TWO, J + 1>(j, w0, w1, sw, p0, p1, acc);
+    if (j == J) c6_chunk<KS, DS, J, NL>(w, sw, pz, acc);
+    else c6_dispatch<KS, DS, NL, J + 1>(j, w, sw, pz, acc);
   }
 }
-
 #ifndef CRT_C6_MINB
-#define CRT_C6_MINB 7  // 72 registers, 7 blocks (28 warps) per SM (8 blocks at 64 registers: 0.5 ms slower)
+#define CRT_C6_MINB (CRT_C6_SLOTS == 3 ? 6 : 7)  // 2 slots: 72 registers, 7 blocks per SM (8 at 64 registers: 0.5 ms slower); 3 slots: 36 KB of shared memory, 6 blocks
 #endif
 template <int KS, int DS>
 __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
@@ -1826,12 +1827,12 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
   constexpr uint32_t PXM = (1u << PXB) - 1;
   constexpr int SEGS = C6_PX / FIN_PX;
   extern __shared__ __align__(16) unsigned char c6_smem[];
-  auto sW = reinterpret_cast<float(*)[C3_SLOTS][C3_THREADS][TK]>(c6_smem);
-  double* sR = reinterpret_cast<double*>(c6_smem + sizeof(float) * 2 * C3_SLOTS * C3_THREADS * TK);
+  auto sW = reinterpret_cast<float(*)[C6_SLOTS][C3_THREADS][TK]>(c6_smem);
+  double* sR = reinterpret_cast<double*>(c6_smem + sizeof(float) * 2 * C6_SLOTS * C3_THREADS * TK);
   uint32_t* s_list = reinterpret_cast<uint32_t*>(reinterpret_cast<unsigned char*>(sR) + sizeof(double) * NR * RWP);
   __shared__ int s_pre[SEGS + 1];
   __shared__ int s_cnt[C6_PX + 1];
-  __shared__ int s_m[C3_SLOTS][C3_THREADS];
+  __shared__ int s_m[C6_SLOTS][C3_THREADS];
   const int nsx = (a.OW + FIN_PX - 1) / FIN_PX;
   const int ngrp = (nsx + SEGS - 1) / SEGS;
   const int grp = blockIdx.x % ngrp;
@@ -1884,12 +1885,12 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
   const int nrows = a.C * KS;  // kernel rows of the chain, (c, ky) ascending
   const double* inblk = a.in + (static_cast<long long>(b) * a.C * a.H + oy) * a.wp + px0;
 
-  for (int base = 0; base < nf; base += C3_THREADS * C3_SLOTS) {
-    int mm[C3_SLOTS], pp[C3_SLOTS];
-    bool live[C3_SLOTS];
-    double acc[C3_SLOTS];
+  for (int base = 0; base < nf; base += C3_THREADS * C6_SLOTS) {
+    int mm[C6_SLOTS], pp[C6_SLOTS];
+    bool live[C6_SLOTS];
+    double acc[C6_SLOTS];
 #pragma unroll
-    for (int c = 0; c < C3_SLOTS; ++c) {
+    for (int c = 0; c < C6_SLOTS; ++c) {
       const int f = base + c * C3_THREADS + tid;
       live[c] = base + c * C3_THREADS + warp * 32 < nf;
       mm[c] = -1;
@@ -1906,8 +1907,8 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
     int loaded = 0;  // kernel rows [0, loaded) are in (or on their way to) the ring
     // this thread's cooperative weight copies, fixed for the pass: global float offset of the
     // 16-byte piece (chain row m, piece pc) and its shared-memory byte offset within a stage
-    constexpr int PIECES = TK / 4, NCOPY = C3_SLOTS * PIECES;
-    constexpr uint32_t STAGE_BYTES = sizeof(float) * C3_SLOTS * C3_THREADS * TK;
+    constexpr int PIECES = TK / 4, NCOPY = C6_SLOTS * PIECES;
+    constexpr uint32_t STAGE_BYTES = sizeof(float) * C6_SLOTS * C3_THREADS * TK;
     int woff[NCOPY];
     uint32_t wsm[NCOPY];
     bool wok[NCOPY];
@@ -1941,8 +1942,9 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
                        "l"(a.w + woff[e] + kc));
       cp_async_commit();
     };
-    const double* p0 = sR + pp[0];
-    const double* p1 = sR + pp[1];
+    const double* pz[C6_SLOTS];
+#pragma unroll
+    for (int c = 0; c < C6_SLOTS; ++c) pz[c] = sR + pp[c];
     const int nper = (nchunks + G::NCH - 1) / G::NCH;
     // the chunk loop, unrolled over a period (every tap offset an immediate); every thread of the
     // block passes the same two barrier sites per chunk (the slot-count branch is inside)
@@ -1958,14 +1960,18 @@ __global__ void __launch_bounds__(C3_THREADS, CRT_C6_MINB)
         cp_async_wait<1>();
         __syncthreads();
         const int sw = (tid >> 2) & 1;
-        if (live[1]) c6_dispatch<KS, DS, true>(jj, &sW[st][0][tid][0], &sW[st][1][tid][0], sw, p0, p1, acc);
-        else if (live[0]) c6_dispatch<KS, DS, false>(jj, &sW[st][0][tid][0], nullptr, sw, p0, nullptr, acc);
+        const float* wr[C6_SLOTS];
+#pragma unroll
+        for (int c = 0; c < C6_SLOTS; ++c) wr[c] = &sW[st][c][tid][0];
+        if (C6_SLOTS > 2 && live[C6_SLOTS > 2 ? 2 : 0]) c6_dispatch<KS, DS, C6_SLOTS>(jj, wr, sw, pz, acc);
+        else if (live[1]) c6_dispatch<KS, DS, 2>(jj, wr, sw, pz, acc);
+        else if (live[0]) c6_dispatch<KS, DS, 1>(jj, wr, sw, pz, acc);
         __syncthreads();
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int c = 0; c < C3_SLOTS; ++c) {
+    for (int c = 0; c < C6_SLOTS; ++c) {
       if (mm[c] < 0) continue;
       const float y = __fadd_rn(__double2float_rn(acc[c]), a.bias[mm[c]]);
       write_out(a.out, a.out_relu, (static_cast<long long>(b) * a.M + mm[c]) * out_plane + static_cast<long long>(oy) * a.owp +
